@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 grid-point updates/s (GLUP/s) of the colour-scheduled sweep.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one pass of the hot path over one batch: the `sweeps` colour-ordered
+sweeps of BASELINE.json config C (default 2: FE9 8194^2, 4 colours, 50
+sweeps), run through the public API `run_sweeps` (one C-ABI sl_sweep call).
+Protocol mirrors the reference bench (bench.py:206-230): seeded init, W
+untimed warm-up steps, K timed steps, CUDA events on the launching stream;
+with N>1 (torchrun) the per-rank time is max-reduced.  Rank 0 prints ONE
+JSON line.  `--impl reference` times the reference algorithm on the host
+cores (the C restatement in oracle/, all threads; the reference itself is
+Python and does not exist on the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1810_04033_b200.configs import BYTES_PER_UPDATE, CONFIGS  # noqa: E402
+
+METRIC = "fp64 grid-point updates/s (GLUP/s)"
+UNIT = "GLUP/s"
+L2_BYTES = 126 * 1024 * 1024
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--per-colour", action="store_true", help="force the unfused K1 path")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload_name):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(workload_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload_config(wl, world, extra=None):
+    grid = "x".join([str(wl.side)] * wl.dim)
+    if wl.batch > 1:
+        grid = f"{wl.batch}x{grid}"
+    grid_bytes = wl.grid_elems * 8
+    cfg = {"workload": wl.name, "baseline_config_index": wl.index, "stencil": wl.stencil,
+           "grid": grid, "sweeps_per_step": wl.sweeps, "update": "form D: u += 0.8*(f - A u)/w_c",
+           "seed": wl.seed,
+           "l2": ("flushed between steps (256 MiB write)" if 2 * grid_bytes < 2 * L2_BYTES
+                  else f"inputs larger than L2 ({2 * grid_bytes / 1e9:.2f} GB u+f)"),
+           "parallelism": "single-gpu" if world == 1 else f"replicas x{world}"}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def cpu_baseline(wl, budget_s=12.0):
+    """Time the C restatement (oracle/, all host threads) on a bounded sample."""
+    import numpy as np
+    from oracle import coracle
+    from oracle import restate as R
+
+    threads = coracle.max_threads()
+    n = wl.n
+    note = "full grid"
+    if wl.dim == 3 and n > 512:
+        n = 512
+        note = "n=512 sub-grid (full 1026^3 u+f would need 17 GB host RAM)"
+    if wl.batch > 1:
+        u, f = R.init_patches(min(wl.batch, 4096), wl.n, wl.seed)
+        note = f"{u.shape[0]} of {wl.batch} patches"
+    else:
+        u = R.init_u(wl.dim, n, wl.seed)
+        f = R.init_f(wl.dim, n, wl.seed + 1)
+    pts = u.size // (n + 2) ** wl.dim * n ** wl.dim
+    t0 = time.perf_counter()
+    coracle.sweep(u, wl.stencil, 1, f=f, omega=wl.omega, form="D", threads=threads)
+    t1 = time.perf_counter()
+    sweeps = 1
+    per = t1 - t0
+    more = max(0, min(wl.sweeps - 1, int(budget_s / max(per, 1e-6)) - 1))
+    if more:
+        coracle.sweep(u, wl.stencil, more, f=f, omega=wl.omega, form="D", threads=threads)
+        sweeps += more
+    t2 = time.perf_counter()
+    del np
+    return {"value": pts * sweeps / (t2 - t0) / 1e9, "unit": UNIT, "cores": threads,
+            "kind": "port",
+            "sample": f"{sweeps} sweep(s) of {wl.stencil} form D on the {note}, "
+                      f"C restatement (oracle/sweep_oracle.c), {threads} pthreads"}
+
+
+def run_reference(args, wl, rank, world):
+    """The reference algorithm on the host cores (C port, all threads)."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import coracle
+    from oracle import restate as R
+
+    threads = coracle.max_threads()
+    n = wl.n
+    note = f"{wl.stencil} full grid"
+    if wl.dim == 3 and n > 512:
+        n = 512
+        note = f"{wl.stencil} n=512 sub-grid of the 1026^3 config"
+    if wl.batch > 1:
+        u, f = R.init_patches(min(wl.batch, 4096), wl.n, wl.seed)
+        note = f"{u.shape[0]} of {wl.batch} patches"
+        pts = u.shape[0] * wl.n ** 2
+    else:
+        u = R.init_u(wl.dim, n, wl.seed)
+        f = R.init_f(wl.dim, n, wl.seed + 1)
+        pts = n ** wl.dim
+    # one step = a bounded sample: as many sweeps as fit ~4 s (>= 1)
+    t0 = time.perf_counter()
+    coracle.sweep(u, wl.stencil, 1, f=f, omega=wl.omega, form="D", threads=threads)
+    per = time.perf_counter() - t0
+    sweeps = max(1, min(wl.sweeps, int(4.0 / max(per, 1e-6))))
+    for _ in range(args.warmup):
+        coracle.sweep(u, wl.stencil, sweeps, f=f, omega=wl.omega, form="D", threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        coracle.sweep(u, wl.stencil, sweeps, f=f, omega=wl.omega, form="D", threads=threads)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = pts * sweeps / (ms / 1e3) / 1e9
+    sample = f"{sweeps} sweep(s) per step of the {note}, form D, C restatement, {threads} pthreads"
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": workload_config(wl, world, {"parallelism": "host cores"}),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    del np
+    print(json.dumps(line), flush=True)
+
+
+def flush_l2(torch, buf):
+    buf.add_(1.0)
+
+
+def run_ours(args, wl, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1810_04033_b200 as sl
+    from paper_1810_04033_b200 import _native
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _native.require_cuda()
+    kind = sl.get_stencil(wl.stencil)
+    flags = _native.SL_FLAG_PER_COLOUR if args.per_colour else 0
+
+    if wl.batch > 1:
+        raise SystemExit("config 5 (batched patches) needs the patch runner")
+    mesh = sl.Mesh(wl.dim, wl.n, device=dev)
+    sl.init(mesh, wl.seed)
+    sl.init_rhs(mesh, wl.seed + 1, wl.omega)
+    cost = sl.CostModel()
+    plan = sl.SweepPlan(mesh, kind, cost)
+    u0_host = mesh.values.copy()
+
+    def step():
+        sl.run_sweeps(mesh, kind, cost, wl.sweeps, plan=plan, flags=flags)
+
+    grid_bytes = wl.grid_elems * 8
+    needs_flush = 2 * grid_bytes < 2 * L2_BYTES
+    flush_buf = torch.zeros(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev) if needs_flush else None
+
+    for _ in range(args.warmup):
+        step()
+    stream = torch.cuda.current_stream(dev)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    launches0 = lib.sl_launch_count()
+    for i in range(args.steps):
+        if flush_buf is not None:
+            flush_l2(torch, flush_buf)
+        starts[i].record(stream)
+        step()
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    launches = lib.sl_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    clock_info = clocks.stop() if clocks else None
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * wl.updates / (ms_per_step / 1e3) / 1e9
+
+    # end to end through the public API with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        f_host = mesh._rhs_host
+        e2e_times = []
+        for i in range(args.steps):
+            mesh.values[:] = u0_host               # host-side prep (untimed)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            mesh.set_rhs(f_host, wl.omega)          # f re-uploaded inside the step
+            step()                                  # uploads u (H2D), sweeps
+            out = mesh.values                       # D2H of the result
+            torch.cuda.synchronize()
+            e2e_times.append(time.perf_counter() - t0)
+            del out
+        te = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * wl.updates / float(te.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * grid_bytes, "d2h_bytes_per_step": grid_bytes}
+
+    if rank != 0:
+        return
+    peak, peak_src = peaks()
+    achieved = BYTES_PER_UPDATE * wl.updates / (ms_per_step / 1e3) / 1e9   # one rank's kernel
+    per_step_launches = launches / args.steps
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded U[0,1) u0, U[-1,1) f)",
+            "config": workload_config(wl, world, {"path": "k1-per-colour" if args.per_colour else "auto"}),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(wl.name),
+                         "peak_source": peak_src,
+                         "algorithmic_bytes": f"{BYTES_PER_UPDATE} B per grid-point update "
+                                              "(u read + f read + u write, once per sweep)",
+                         "launches_per_step": per_step_launches},
+            "gpu_launches": int(launches),
+            "clocks": clock_info,
+            "e2e": e2e}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    wl = CONFIGS[args.config]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    try:
+        if args.impl == "reference":
+            run_reference(args, wl, rank, world)
+        else:
+            run_ours(args, wl, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

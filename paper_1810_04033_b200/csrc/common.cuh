@@ -1,0 +1,111 @@
+// common.cuh — stencil shapes, kernel parameters and the per-point update
+// arithmetic shared by every sweep kernel (K1 per-colour, K2 fused, K3 patch).
+//
+// Bitwise contract (oracle/restate.py):
+//   Form R (reference kernels.py:224-232):
+//       acc = +0.0; for j in canonical order: acc = acc + |w_j|*u_j; u_c = acc / w_c
+//   Form D (BASELINE configs, defined in oracle/restate.py):
+//       Au = w_c*u_c; for j: Au = Au + w_j*u_j; u_c = u_c + omega*((f_c - Au)/w_c)
+// Every operation is an explicitly rounded __d*_rn intrinsic, so nvcc can
+// neither contract a multiply-add into an FMA nor reassociate.  Two exact
+// rewrites are used: |w|=1 -> the multiply is dropped (1*x == x, and
+// Au + (-1*x) == Au - x bit for bit), and a power-of-two w_c divides by
+// multiplying with its exact reciprocal.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sl {
+
+// bench evidence: kernels launched by this library (capi.cu)
+void note_launch(int n = 1);
+
+// Internal shape ids: the four reference neighbour sets plus Q1 = FE27 with
+// all six face weights zero (BASELINE config 4), which skips the faces.
+enum Shape : int { FD5 = 0, FE9 = 1, FD7 = 2, FE27 = 3, Q1 = 4 };
+
+struct Off {
+  int x, y, z;
+};
+
+__host__ __device__ constexpr int shape_dim(int s) { return (s == FD5 || s == FE9) ? 2 : 3; }
+
+__host__ __device__ constexpr bool shape_keeps(int s, int dx, int dy, int dz) {
+  return (dx == 0 && dy == 0 && dz == 0) ? false
+         : (shape_dim(s) == 2 && dz != 0) ? false
+         : (s == FD5 || s == FD7)         ? ((dx != 0) + (dy != 0) + (dz != 0)) == 1
+         : (s == Q1)                      ? ((dx != 0) + (dy != 0) + (dz != 0)) >= 2
+                                          : true;
+}
+
+// Number of neighbours of shape s.
+__host__ __device__ constexpr int shape_nnz(int s) {
+  int c = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) c += shape_keeps(s, dx, dy, dz) ? 1 : 0;
+  return c;
+}
+
+// j-th neighbour in canonical order = lexicographic in (dz, dy, dx)
+// = sorted by reversed displacement = ascending flat delta (kernels.py:78-80).
+__host__ __device__ constexpr Off shape_off(int s, int j) {
+  int c = 0;
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx)
+        if (shape_keeps(s, dx, dy, dz)) {
+          if (c == j) return Off{dx, dy, dz};
+          ++c;
+        }
+  return Off{0, 0, 0};
+}
+
+enum DivMode : int { DIV_IEEE = 0, DIV_POW2 = 1 };
+
+struct Params {
+  double *u;
+  const double *f;
+  int32_t *status;
+  int64_t nx, ny, nz;  // interior extents (nz = 1 in 2D)
+  int64_t sy, sz;      // element strides of y and z
+  int64_t batch, bstride;
+  int32_t px, py, pz;  // origin parities
+  int32_t colours;
+  double w[26];   // signed weights, compact canonical order of the kernel shape
+  double aw[26];  // |w|
+  double wc, rwc, omega;
+  int64_t delta[26];  // flat deltas (update_cells / residual)
+};
+
+template <int FORM, bool UNIT, int DIV>
+__device__ __forceinline__ double div_wc(double a, const Params &p) {
+  if (DIV == DIV_POW2) return __dmul_rn(a, p.rwc);  // exact: w_c is a power of two
+  return __ddiv_rn(a, p.wc);
+}
+
+// Accumulator helpers: feed neighbours one at a time in canonical order.
+template <int FORM, bool UNIT>
+__device__ __forceinline__ double acc_init(double uc, const Params &p) {
+  return FORM == 0 ? 0.0 : __dmul_rn(p.wc, uc);
+}
+
+template <int FORM, bool UNIT>
+__device__ __forceinline__ double acc_add(double acc, double v, int j, const Params &p) {
+  if (FORM == 0) return __dadd_rn(acc, UNIT ? v : __dmul_rn(p.aw[j], v));
+  return UNIT ? __dsub_rn(acc, v) : __dadd_rn(acc, __dmul_rn(p.w[j], v));
+}
+
+template <int FORM, bool UNIT, int DIV>
+__device__ __forceinline__ double acc_finish(double acc, double uc, double fc, const Params &p) {
+  if (FORM == 0) return div_wc<FORM, UNIT, DIV>(acc, p);
+  double q = div_wc<FORM, UNIT, DIV>(__dsub_rn(fc, acc), p);
+  return __dadd_rn(uc, __dmul_rn(p.omega, q));
+}
+
+__device__ __forceinline__ bool finite64(double v) {
+  // exponent bits not all ones
+  return (__double_as_longlong(v) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
+}
+
+}  // namespace sl

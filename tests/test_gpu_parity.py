@@ -1,0 +1,252 @@
+"""GPU parity: the CUDA path against the reference (golden digests) and the
+oracle (C / NumPy restatements), bit for bit.
+
+Everything here calls the sm_100a library through the C ABI (via the
+drop-in Python surface) and compares against tests/golden/ or oracle/.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1810_04033_b200 as sl
+from oracle import coracle
+from oracle import restate as R
+from paper_1810_04033_b200 import _native, strategies
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+ALL = list(R.STENCIL_TABLE)
+
+
+def _digest(arr):
+    return hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest()
+
+
+def _bits_equal(a, b):
+    return np.array_equal(np.asarray(a).reshape(-1).view(np.int64), np.asarray(b).reshape(-1).view(np.int64))
+
+
+def _parse(key):
+    parts = dict(p.split("=") for p in key.split("/")[1:])
+    return key.split("/")[0], int(parts["n"]), int(parts["s"]), int(parts["seed"]), float(parts.get("b", 0.0))
+
+
+@pytest.fixture(scope="module")
+def ref_digests():
+    with open(os.path.join(GOLDEN, "reference_digests.json")) as fh:
+        return json.load(fh)
+
+
+# -- Form R vs the reference itself ------------------------------------------
+
+@pytest.mark.parametrize("path", ["fused", "per_sweep", "reference_k1"])
+def test_form_r_matches_reference_digests(ref_digests, path):
+    """Acceptance criterion 5 digests (reference tests/test_acceptance.py:107-130)."""
+    for key, want in ref_digests["sweeps"].items():
+        name, n, sweeps, seed, b = _parse(key)
+        kind = sl.get_stencil(name)
+        with sl.StrategyRunner(kind.dim, n, kind, sl.CostModel(), "colouring", seed=seed,
+                               boundary=b) as r:
+            r.reinit()
+            if path == "fused":
+                r.run_sweeps(sweeps)
+            elif path == "per_sweep":
+                for _ in range(sweeps):
+                    r.sweep()
+            else:
+                for _ in range(sweeps):
+                    sl.sweep_colouring_reference(r.mesh, kind, sl.CostModel())
+            assert r.digest() == want, (key, path)
+
+
+def test_form_r_small_buffers_bitwise():
+    small = np.load(os.path.join(GOLDEN, "reference_small.npz"))
+    for name in ("fd5", "fe9", "fd7", "fe27"):
+        kind = sl.get_stencil(name)
+        n = 10 if kind.dim == 2 else 6
+        m = sl.make_mesh(kind.dim, n, seed=11)
+        for strat in ("colouring", "hyb-sync", "hyb-depend"):
+            m2 = sl.make_mesh(kind.dim, n, seed=11)
+            for _ in range(5):
+                sl.run_sweep(strat, m2, kind, sl.CostModel(), pool=sl.DevicePool())
+            assert _bits_equal(m2.values, small[name]), (name, strat)
+        sl.run_sweeps(m, kind, sl.CostModel(), 5)
+        assert _bits_equal(m.values, small[name]), name
+
+
+# -- Form D / Q1 vs the oracle (self-pinned) ----------------------------------
+
+def _oracle_d(name, n, sweeps, seed=42, boundary=0.0):
+    dim = R.STENCIL_TABLE[name][0]
+    u = R.init_u(dim, n, seed, boundary)
+    f = R.init_f(dim, n, seed + 1)
+    coracle.sweep(u, name, sweeps, f=f, omega=0.8, form="D")
+    return u
+
+
+def _gpu_d(name, n, sweeps, seed=42, boundary=0.0, mode="fused"):
+    kind = sl.get_stencil(name)
+    m = sl.make_mesh(kind.dim, n, seed=seed, boundary_value=boundary)
+    sl.init_rhs(m, seed + 1, 0.8)
+    if mode == "fused":
+        sl.run_sweeps(m, kind, sl.CostModel(), sweeps)
+    elif mode == "k1":
+        sl.run_sweeps(m, kind, sl.CostModel(), sweeps, flags=_native.SL_FLAG_PER_COLOUR)
+    else:
+        for _ in range(sweeps):
+            sl.sweep_colouring(sl.DevicePool(), m, kind, sl.CostModel())
+    return m.values
+
+
+@pytest.mark.parametrize("name", ALL)
+@pytest.mark.parametrize("mode", ["fused", "k1", "single"])
+def test_form_d_matches_oracle_small_and_ragged(name, mode):
+    dim = R.STENCIL_TABLE[name][0]
+    sizes = (1, 2, 3, 7, 16, 33, 64, 130) if dim == 2 else (1, 2, 3, 5, 8, 17, 32)
+    for n in sizes:
+        for sweeps in (1, 2, 5):
+            want = _oracle_d(name, n, sweeps, seed=n)
+            got = _gpu_d(name, n, sweeps, seed=n, mode=mode)
+            assert _bits_equal(got, want), (name, n, sweeps, mode)
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_form_r_all_kinds_vs_oracle_ragged(name):
+    dim = R.STENCIL_TABLE[name][0]
+    kind = sl.get_stencil(name)
+    for n in ((1, 4, 9, 31, 100) if dim == 2 else (1, 4, 9, 21)):
+        u = R.init_u(dim, n, 3, 0.25)
+        R.sweep(u, name, 3)
+        m = sl.make_mesh(dim, n, seed=3, boundary_value=0.25)
+        sl.run_sweeps(m, kind, sl.CostModel(), 3)
+        assert _bits_equal(m.values, u), (name, n)
+
+
+# -- BASELINE configs at full size (property: equals the C oracle) ------------
+
+def test_config1_fd5_1026_full():
+    want = _oracle_d("fd5", 1024, 100)
+    got = _gpu_d("fd5", 1024, 100)
+    assert _bits_equal(got, want)
+
+
+def test_config2_fe9_8194_full():
+    want = _oracle_d("fe9", 8192, 50)
+    got = _gpu_d("fe9", 8192, 50)
+    assert _bits_equal(got, want)
+
+
+def test_config3_fd7_514_full():
+    want = _oracle_d("fd7", 512, 20)
+    got = _gpu_d("fd7", 512, 20)
+    assert _bits_equal(got, want)
+
+
+def test_config4_fe27q1_1026_two_sweeps():
+    # full 1026^3 grid; 2 of the 10 sweeps keep the CPU oracle to ~a minute
+    want = _oracle_d("fe27q1", 1024, 2)
+    got = _gpu_d("fe27q1", 1024, 2)
+    assert _bits_equal(got, want)
+
+
+# -- reference unit behaviours on the device -----------------------------------
+
+def test_update_cells_batch_equals_oracle_colour_pass():
+    for name in ALL:
+        kind = sl.get_stencil(name)
+        n = 6 if kind.dim == 2 else 4
+        m = sl.make_mesh(kind.dim, n, seed=5)
+        plan = sl.SweepPlan(m, kind, sl.CostModel())
+        sl.update_cells_batch(m, kind, plan.colour_cells[0], 0)
+        u = R.init_u(kind.dim, n, 5)
+        R.colour_pass(u, name, 0)
+        assert _bits_equal(m.values, u), name
+
+
+def test_update_cell_known_answers():
+    m = sl.Mesh(2, 3)
+    m.values.fill(1.0)
+    assert sl.update_cell(m, sl.FD5, (2, 2)) == 1.0
+    m = sl.Mesh(2, 3)
+    m.values[m.flat_index((2, 1))] = 1.0
+    assert sl.update_cell(m, sl.FD5, (2, 2)) == 0.25
+    with pytest.raises(IndexError):
+        sl.update_cell(m, sl.FD5, (0, 1))
+
+
+def test_nonfinite_raises_numerics_error():
+    m = sl.make_mesh(2, 8, seed=1)
+    m.values[m.flat_index((1, 2))] = np.inf
+    with pytest.raises(sl.NumericsError):
+        sl.run_sweeps(m, sl.FD5, sl.CostModel(), 2)
+    m = sl.make_mesh(2, 4, seed=1)
+    m.values[m.flat_index((0, 1))] = np.nan
+    with pytest.raises(sl.NumericsError):
+        sl.update_cells_batch(m, sl.FD5, np.array([m.flat_index((1, 1))]), 0)
+
+
+def test_constant_mesh_unchanged():
+    for kind in (sl.FD5, sl.FE27):
+        m = sl.Mesh(kind.dim, 4)
+        m.values.fill(1.75)
+        sl.run_sweep("colouring", m, kind, sl.CostModel(), pool=sl.DevicePool())
+        assert (m.values == 1.75).all()
+
+
+def test_halo_immutable():
+    for name in ALL:
+        kind = sl.get_stencil(name)
+        n = 9 if kind.dim == 2 else 6
+        m = sl.make_mesh(kind.dim, n, seed=2, boundary_value=3.25)
+        sl.init_rhs(m, 3)
+        halo = m.halo_flat()
+        sl.run_sweeps(m, kind, sl.CostModel(), 4)
+        assert (m.values[halo] == 3.25).all(), name
+
+
+def test_residual_matches_reference(ref_digests):
+    for key, want in ref_digests["residual"].items():
+        name = key.split("/")[0]
+        kind = sl.get_stencil(name)
+        n = 10 if kind.dim == 2 else 6
+        assert sl.residual_max(sl.make_mesh(kind.dim, n, seed=9), kind).hex() == want, key
+
+
+def test_residual_form_d_and_decrease():
+    m = sl.make_mesh(2, 33, seed=7)
+    sl.init_rhs(m, 8)
+    f = R.init_f(2, 33, 8)
+    r0 = sl.residual_max(m, sl.FD5)
+    assert r0 == R.residual_max(R.init_u(2, 33, 7), "fd5", f=f)
+    sl.run_sweeps(m, sl.FD5, sl.CostModel(), 50)
+    assert sl.residual_max(m, sl.FD5) < r0
+
+
+def test_merged_colour_negative_control_mismatches():
+    """Reference bench.py:372-395: the racy single-pass variant must be caught."""
+    kind = sl.FD5
+    want = R.init_u(2, 64, 1)
+    R.sweep(want, "fd5", 1)
+    m = sl.make_mesh(2, 64, seed=1)
+    sl.sweep_colouring(sl.DevicePool(), m, kind, sl.CostModel(), _fault_merge_colours=True)
+    assert not _bits_equal(m.values, want)
+
+
+def test_deterministic_across_repeats_and_paths():
+    digests = set()
+    for mode in ("fused", "k1", "single", "fused"):
+        digests.add(_digest(_gpu_d("fe27q1", 20, 3, mode=mode)))
+    assert len(digests) == 1
+
+
+def test_host_edits_between_sweeps_are_seen():
+    m = sl.make_mesh(2, 6, seed=4)
+    sl.run_sweeps(m, sl.FD5, sl.CostModel(), 1)
+    m.values.fill(2.0)
+    sl.run_sweeps(m, sl.FD5, sl.CostModel(), 1)
+    assert (m.values == 2.0).all()
