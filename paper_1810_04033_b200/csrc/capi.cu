@@ -82,8 +82,11 @@ static int resolve(const sl_stencil *s, int dim, KernelKey *key, Params *p) {
   key->shape = shape;
   key->form = s->form;
   key->unit = unit;
-  key->div = is_pow2(std::fabs(s->wc)) ? DIV_POW2 : DIV_IEEE;
-  p->rwc = 1.0 / s->wc;  // exact when DIV_POW2
+  // rwc = RN(1/w_c): exact for a power of two, the Markstein seed otherwise
+  key->div = is_pow2(std::fabs(s->wc)) ? DIV_POW2
+             : (s->wc > 0.0 && std::isnormal(s->wc) && std::isnormal(1.0 / s->wc)) ? DIV_RCP
+                                                                                  : DIV_IEEE;
+  p->rwc = 1.0 / s->wc;
   return SL_OK;
 }
 

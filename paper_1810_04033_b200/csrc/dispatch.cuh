@@ -14,8 +14,9 @@ struct KernelKey {
 
 template <int S, int F, bool U, typename Fn>
 cudaError_t dispatch_div(int div, Fn &&fn) {
-  return div == DIV_POW2 ? fn.template operator()<S, F, U, DIV_POW2>()
-                         : fn.template operator()<S, F, U, DIV_IEEE>();
+  if (div == DIV_POW2) return fn.template operator()<S, F, U, DIV_POW2>();
+  if (div == DIV_RCP) return fn.template operator()<S, F, U, DIV_RCP>();
+  return fn.template operator()<S, F, U, DIV_IEEE>();
 }
 
 template <int S, int F, typename Fn>

@@ -8,16 +8,17 @@
 // ever reads a value another tile already overwrote):
 //   * a CTA owns a tile of the non-streaming axes (3D: TX x TY columns,
 //     2D: TX columns) and a chunk of the streaming axis (z / y);
-//   * it streams planes (3D) / row blocks (2D) of the tile plus a ghost
-//     margin through a circular shared-memory window.  Global loads are
-//     16-byte coalesced (LDG.128) one step ahead into registers, then
-//     stored DE-INTERLEAVED by x parity (even x | odd x halves), so that
-//     the 32 lanes of a warp updating one colour — every other x — hit 32
-//     consecutive 8-byte words (conflict-free), and so do their x+-1
-//     neighbours;
-//   * each phase k updates its colour's points on plane t - lag[k] in
-//     place in shared memory, redundantly on the ghost margin need[k]
-//     (plan.cuh), f is read straight from global (L1-cached, used once);
+//   * it streams planes (3D) / row blocks (2D) of u and f for the tile plus
+//     a ghost margin through circular shared-memory windows.  Global loads
+//     are 16-byte coalesced (LDG.128), issued one step ahead into registers
+//     and stored DE-INTERLEAVED by x parity (even-x half | odd-x half) at
+//     the start of the next step, so the 32 lanes of a warp updating one
+//     colour (every other x) and their x+-1 neighbours each hit 32
+//     consecutive 8-byte words: conflict-free;
+//   * phase k updates its colour's points on plane t - lag[k] in place in
+//     shared memory, redundantly on the ghost margin need[k] (plan.cuh).  A
+//     warp item is a 32-lane strip x RY point rows whose neighbour rows are
+//     loaded once and shared (register blocking), all loads before any store;
 //   * finished planes of the owned box are written to `dst` with STG.128.
 // The per-point arithmetic is common.cuh's, in canonical neighbour order,
 // so the result is bitwise identical to the per-colour path and the oracle.
@@ -34,9 +35,9 @@ __host__ __device__ constexpr int natural_colours(int s) {
 
 __host__ __device__ constexpr int even_up(int v) { return (v + 1) & ~1; }
 
-// start of tile k of n over [0, len) — even, non-decreasing, last = len
+// start of tile k of n over [0, len) — even, non-decreasing, last = len (len even)
 __host__ __device__ inline int64_t tile_start(int64_t k, int64_t len, int64_t n) {
-  return 2 * ((k * (len / 2)) / n);  // len is even (checked on the host)
+  return 2 * ((k * (len / 2)) / n);
 }
 
 __host__ __device__ inline int64_t chunk_start(int64_t k, int64_t len, int64_t n) {
@@ -45,13 +46,7 @@ __host__ __device__ inline int64_t chunk_start(int64_t k, int64_t len, int64_t n
 
 __device__ __forceinline__ double2 ldg_nc2(const double *p) {
   double2 v;
-  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
-
-__device__ __forceinline__ double ldg_nc(const double *p) {
-  double v;
-  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
 
@@ -66,6 +61,7 @@ template <int S, int M>
 struct Geo3 {
   static constexpr FPlan P = make_plan(S, natural_colours(S), M);
   static constexpr int K = P.K, C = P.C, LAGMAX = P.lagmax;
+  static constexpr bool RB = (P.C == 2);
   static constexpr int GX = even_up(P.load[0]);
   static constexpr int GY = P.load[1];
   static constexpr int GZ = P.load[2];
@@ -75,13 +71,20 @@ struct Geo3 {
   static constexpr int PY = 32;
   static constexpr int TX = PX - 2 * GX;
   static constexpr int TY = PY - 2 * GY;
-  static constexpr int W = LAGMAX + 4;       // plane slots in the window
+  static constexpr int W = LAGMAX + 3;       // u plane slots
+  static constexpr int WF = LAGMAX + 1;      // f plane slots
   static constexpr int SLOT = PY * ROWW;
+  static constexpr int RSTEP = RB ? 1 : 2;   // point rows of one colour
+  static constexpr int RY = RB ? 4 : 2;      // point rows per warp item
+  static constexpr int MINB = (S == Q1 || S == FE27) ? 1 : 2;  // CTAs/SM (register budget)
+  static constexpr int PAD_ROWS = (RY - 1) * RSTEP + 2;
   static constexpr int NT = 256;
   static constexpr int NW = NT / 32;
   static constexpr int PAIRS = PY * PX / 2;
   static constexpr int LPT = PAIRS / NT;
-  static constexpr size_t SMEM = size_t(W) * SLOT * sizeof(double);
+  static constexpr int UOFF = 0;
+  static constexpr int FOFF = W * SLOT;
+  static constexpr size_t SMEM = size_t((W + WF) * SLOT + PAD_ROWS * ROWW) * sizeof(double);
   static_assert(PAIRS % NT == 0, "plane load split");
   static_assert(TX >= 8 && TY >= 4, "ghost margin too wide for the tile");
 };
@@ -90,6 +93,7 @@ template <int S, int M>
 struct Geo2 {
   static constexpr FPlan P = make_plan(S, natural_colours(S), M);
   static constexpr int K = P.K, C = P.C, LAGMAX = P.lagmax;
+  static constexpr bool RB = (P.C == 2);
   static constexpr int GX = even_up(P.load[0]);
   static constexpr int GY = P.load[1];       // streaming-axis margin
   static constexpr int NSTRIP = 4;
@@ -97,14 +101,19 @@ struct Geo2 {
   static constexpr int HW = PX / 2 + 2;
   static constexpr int ROWW = 2 * HW;
   static constexpr int R = 8;                // rows per macro-step
-  static constexpr int NB = 4;               // row blocks in the window
+  static constexpr int NB = 3;               // u row blocks resident
+  static constexpr int NBF = 2;              // f row blocks resident
   static constexpr int WR = NB * R;
+  static constexpr int WRF = NBF * R;
   static constexpr int TX = PX - 2 * GX;
+  static constexpr int RSTEP = RB ? 1 : 2;
+  static constexpr int RY = 2;
   static constexpr int NT = 256;
   static constexpr int NW = NT / 32;
   static constexpr int PAIRS = R * PX / 2;
   static constexpr int LPT = PAIRS / NT;
-  static constexpr size_t SMEM = size_t(WR) * ROWW * sizeof(double);
+  static constexpr int FOFF = WR * ROWW;
+  static constexpr size_t SMEM = size_t((WR + WRF) * ROWW) * sizeof(double);
   static_assert(LAGMAX + 1 <= R, "row block shorter than the phase lag");
   static_assert(PAIRS % NT == 0, "block load split");
 };
@@ -113,81 +122,113 @@ struct Tiles {
   int64_t ntx, nty, nzc;  // tiles along x, y (3D) and chunks along the streaming axis
 };
 
-// offsets, relative to (row base + lane i), of the x-1 / x / x+1 neighbours
-// of a point at local x = 2i + s in the de-interleaved row layout
+// Offset (relative to row base + lane) of the x+dx neighbour of a point at
+// local x = 2*lane + s in a de-interleaved row [pad, even.., pad | pad, odd.., pad].
 template <int HW>
-struct XOff {
-  int m, c, p;
-  __device__ __forceinline__ XOff(int s)
-      : m((1 - s) * HW + s), c(s * HW + 1), p((1 - s) * HW + 1 + s) {}
-  __device__ __forceinline__ int at(int dx) const { return dx < 0 ? m : (dx == 0 ? c : p); }
-};
+__host__ __device__ constexpr int xoff(int s, int dx) {
+  return (((s + dx) & 1) ? HW : 0) + 1 + ((s + dx) >> 1);
+}
+
+// ---------------------------------------------------------------------------
+// one warp item: RY point rows of a 32-lane strip.
+//   rowoff[dz+1][k]: smem element offset of source row k (point row r uses
+//   k = r*RSTEP + dy + 1), lane included.  s0: x parity of row 0's points.
+// All loads happen before any store, so repeated (row, x) loads are CSE'd.
+
+template <int S, int FORM, bool UNIT, int DIV, int RY, int RSTEP, bool RB, int HW, int S0,
+          typename RowOff, typename FOff>
+__device__ __forceinline__ int update_item(double *sm, const RowOff &rowoff, const FOff &foff,
+                                           unsigned vmask, const Params &p) {
+  constexpr int NNZ = shape_nnz(S);
+  double out[RY];
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    const int s = RB ? (S0 ^ ((r * RSTEP) & 1)) : S0;
+    const int kc = r * RSTEP + 1;
+    const double uc = sm[rowoff(1, kc) + (s ? xoff<HW>(1, 0) : xoff<HW>(0, 0))];
+    double acc = acc_init<FORM, UNIT>(uc, p);
+#pragma unroll
+    for (int q = 0; q < NNZ; ++q) {
+      const Off o = shape_off(S, q);
+      const int off = s ? xoff<HW>(1, o.x) : xoff<HW>(0, o.x);
+      acc = acc_add<FORM, UNIT>(acc, sm[rowoff(o.z + 1, kc + o.y) + off], q, p);
+    }
+    double fc = 0.0;
+    if (FORM == 1) fc = sm[foff(r) + (s ? xoff<HW>(1, 0) : xoff<HW>(0, 0))];
+    out[r] = acc_finish<FORM, UNIT, DIV>(acc, uc, fc, p);
+  }
+  int bad = 0;
+#pragma unroll
+  for (int r = 0; r < RY; ++r) {
+    const int s = RB ? (S0 ^ ((r * RSTEP) & 1)) : S0;
+    if (vmask & (1u << r)) {
+      bad |= !finite64(out[r]);
+      sm[rowoff(1, r * RSTEP + 1) + (s ? xoff<HW>(1, 0) : xoff<HW>(0, 0))] = out[r];
+    }
+  }
+  return bad;
+}
 
 // ---------------------------------------------------------------------------
 // 3D: z-streaming over (TX x TY) tiles
 
 template <int S, int FORM, bool UNIT, int DIV, int M>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, Geo3<S, M>::MINB)
 k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, Tiles tl) {
   using G = Geo3<S, M>;
   constexpr FPlan P = G::P;
-  constexpr int NNZ = shape_nnz(S);
   extern __shared__ double sm[];
 
-  const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
-  const int64_t item = blockIdx.x;
-  const int64_t tx = item % tl.ntx;
-  const int64_t ty = (item / tl.ntx) % tl.nty;
-  const int64_t zc = item / (tl.ntx * tl.nty);
-  const int64_t x0 = tile_start(tx, Sx, tl.ntx), x1 = tile_start(tx + 1, Sx, tl.ntx);
-  const int64_t y0 = chunk_start(ty, Sy, tl.nty), y1 = chunk_start(ty + 1, Sy, tl.nty);
-  const int64_t z0 = chunk_start(zc, Sz, tl.nzc), z1 = chunk_start(zc + 1, Sz, tl.nzc);
-  const int TXo = (int)(x1 - x0), TYo = (int)(y1 - y0);
-  const int64_t gx0 = x0 - G::GX, gy0 = y0 - G::GY;
+  const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2, Sz = (int)p.nz + 2;
+  const int item = blockIdx.x;
+  const int tx = item % (int)tl.ntx;
+  const int ty = (item / (int)tl.ntx) % (int)tl.nty;
+  const int zc = item / (int)(tl.ntx * tl.nty);
+  const int x0 = (int)tile_start(tx, Sx, tl.ntx), x1 = (int)tile_start(tx + 1, Sx, tl.ntx);
+  const int y0 = (int)chunk_start(ty, Sy, tl.nty), y1 = (int)chunk_start(ty + 1, Sy, tl.nty);
+  const int z0 = (int)chunk_start(zc, Sz, tl.nzc), z1 = (int)chunk_start(zc + 1, Sz, tl.nzc);
+  const int TXo = x1 - x0, TYo = y1 - y0;
+  const int gx0 = x0 - G::GX, gy0 = y0 - G::GY;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int base_par = (int)((gx0 - 1 + p.px) & 1);
+  const int base_par = (gx0 - 1 + p.px) & 1;
 
-  auto slot_of = [](int64_t gz) -> int { return (int)((gz % G::W + G::W) % G::W); };
+  auto uslot = [](int gz) -> int { return ((gz % G::W) + G::W) % G::W * G::SLOT; };
+  auto fslot = [](int gz) -> int { return G::FOFF + ((gz % G::WF) + G::WF) % G::WF * G::SLOT; };
 
-  // register-staged plane load (16-byte coalesced), then de-interleaved STS
-  auto load_regs = [&](int64_t gz, double2 (&r)[G::LPT]) {
+  auto load_regs = [&](const double *base, int gz, double2 (&r)[G::LPT]) {
 #pragma unroll
     for (int k = 0; k < G::LPT; ++k) {
       const int pair = tid + k * G::NT;
       const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      const int64_t gx = gx0 + 2 * i, gy = gy0 + row;
+      const int gx = gx0 + 2 * i, gy = gy0 + row;
       const bool ok = gz >= 0 && gz < Sz && gy >= 0 && gy < Sy && gx >= 0 && gx < Sx;
-      r[k] = ok ? ldg_nc2(src + gz * p.sz + gy * p.sy + gx) : make_double2(0.0, 0.0);
+      r[k] = ok ? ldg_nc2(base + (int64_t)gz * p.sz + (int64_t)gy * p.sy + gx) : make_double2(0.0, 0.0);
     }
   };
-  auto store_regs = [&](int64_t gz, const double2 (&r)[G::LPT]) {
-    double *slot = sm + slot_of(gz) * G::SLOT;
+  auto store_regs = [&](int off, const double2 (&r)[G::LPT]) {
 #pragma unroll
     for (int k = 0; k < G::LPT; ++k) {
       const int pair = tid + k * G::NT;
       const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      slot[row * G::ROWW + 1 + i] = r[k].x;
-      slot[row * G::ROWW + G::HW + 1 + i] = r[k].y;
+      sm[off + row * G::ROWW + 1 + i] = r[k].x;
+      sm[off + row * G::ROWW + G::HW + 1 + i] = r[k].y;
     }
   };
 
-  const int64_t t_begin = z0 - G::GZ - 1;
-  const int64_t t_end = z1 - 1 + G::LAGMAX;
-  {
-    double2 r[G::LPT];
-    load_regs(t_begin + 1, r);
-    store_regs(t_begin + 1, r);
-    load_regs(t_begin + 2, r);
-    store_regs(t_begin + 2, r);
-  }
-  __syncthreads();
+  const int t_begin = z0 - G::GZ - 1;
+  const int t_end = z1 - 1 + G::LAGMAX;
+  double2 pu[G::LPT], pf[G::LPT];
+  load_regs(src, t_begin + 1, pu);
+  if (FORM == 1) load_regs(p.f, t_begin, pf);
 
   int bad = 0;
-  for (int64_t t = t_begin; t <= t_end; ++t) {
-    double2 pf[G::LPT];
-    const int64_t gz_pf = t + 2;
-    const bool do_pf = gz_pf < z1 + G::GZ;
-    if (do_pf) load_regs(gz_pf, pf);
+  for (int t = t_begin; t <= t_end; ++t) {
+    // planes loaded during the previous step go into their (free) slots
+    if (t + 1 < z1 + G::GZ) store_regs(uslot(t + 1), pu);
+    if (FORM == 1 && t < z1 + G::GZ) store_regs(fslot(t), pf);
+    __syncthreads();
+    if (t + 2 < z1 + G::GZ) load_regs(src, t + 2, pu);
+    if (FORM == 1 && t + 1 < z1 + G::GZ) load_regs(p.f, t + 1, pf);
 
     // ---- colour phases, in order ----
     [&]<int... Js>(std::integer_sequence<int, Js...>) {
@@ -196,50 +237,48 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
             constexpr int J = Js;
             constexpr int c = P.colour[J];
             constexpr int nx_ = P.need[J][0], ny_ = P.need[J][1], nz_ = P.need[J][2];
-            const int64_t pz = t - P.lag[J];
-            bool active = pz >= 1 && pz <= p.nz && pz >= z0 - nz_ && pz < z1 + nz_;
-            const int qz = (int)((pz - 1 + p.pz) & 1);
-            if (G::C == 8 && qz != ((c >> 2) & 1)) active = false;
-            if (!active) return;
-            const double *sl_m = sm + slot_of(pz - 1) * G::SLOT;
-            double *sl_c = sm + slot_of(pz) * G::SLOT;
-            const double *sl_p = sm + slot_of(pz + 1) * G::SLOT;
-            // point rows of this phase (local slot rows)
-            int ly_lo = G::GY - ny_, ly_hi = G::GY + TYo + ny_;  // [lo, hi)
-            if (gy0 + ly_lo < 1) ly_lo = (int)(1 - gy0);
-            if (gy0 + ly_hi > p.ny + 1) ly_hi = (int)(p.ny + 1 - gy0);
-            int rstep = 1;
-            if (G::C != 2) {
-              rstep = 2;
-              const int want = (c >> 1) & 1;
-              if ((int)((gy0 + ly_lo - 1 + p.py) & 1) != want) ++ly_lo;
-            }
+            const int pz = t - P.lag[J];
+            if (pz < 1 || pz > (int)p.nz || pz < z0 - nz_ || pz >= z1 + nz_) return;
+            const int qz = (pz - 1 + p.pz) & 1;
+            if (!G::RB && ((c >> 2) & 1) != qz) return;
+            int ly_lo = G::GY - ny_, ly_hi = G::GY + TYo + ny_;
+            if (gy0 + ly_lo < 1) ly_lo = 1 - gy0;
+            if (gy0 + ly_hi > (int)p.ny + 1) ly_hi = (int)p.ny + 1 - gy0;
+            if (!G::RB && (((gy0 + ly_lo - 1 + p.py) & 1) != ((c >> 1) & 1))) ++ly_lo;
+            const int npr = ly_hi > ly_lo ? (ly_hi - ly_lo + G::RSTEP - 1) / G::RSTEP : 0;
+            const int nitems = (npr + G::RY - 1) / G::RY;
             const int lx_lo = G::GX - nx_, lx_hi = G::GX + TXo + nx_;
-            for (int ly = ly_lo + warp * rstep; ly < ly_hi; ly += G::NW * rstep) {
-              const int64_t gy = gy0 + ly;
-              const int qy = (int)((gy - 1 + p.py) & 1);
-              const int qxt = G::C == 2 ? ((c + qy + qz) & 1) : (c & 1);
-              const int s = (qxt ^ base_par) & 1;
-              const int lx = 2 * lane + s;
-              const int64_t gx = gx0 + lx;
-              const bool valid = lx >= lx_lo && lx < lx_hi && gx >= 1 && gx <= p.nx;
-              double fc = 0.0;
-              if (FORM == 1 && valid) fc = ldg_nc(p.f + pz * p.sz + gy * p.sy + gx);
-              const XOff<G::HW> xo(s);
-              const int rb = ly * G::ROWW + lane;
-              const double uc = sl_c[rb + xo.c];
-              double acc = acc_init<FORM, UNIT>(uc, p);
+            const int um = uslot(pz - 1), uc = uslot(pz), up = uslot(pz + 1);
+            const int fo = fslot(pz);
+            for (int it = warp; it < nitems; it += G::NW) {
+              const int ly0 = ly_lo + it * G::RY * G::RSTEP;
+              const int gy = gy0 + ly0;
+              const int qy = (gy - 1 + p.py) & 1;
+              const int qxt = G::RB ? ((c + qy + qz) & 1) : (c & 1);
+              const int s0 = (qxt ^ base_par) & 1;
+              const int gxl = gx0 + 2 * lane;  // global x of the lane's even column
+              unsigned vmask = 0;
 #pragma unroll
-              for (int q = 0; q < NNZ; ++q) {
-                const Off o = shape_off(S, q);
-                const double *pl = o.z < 0 ? sl_m : (o.z > 0 ? sl_p : sl_c);
-                acc = acc_add<FORM, UNIT>(acc, pl[rb + o.y * G::ROWW + xo.at(o.x)], q, p);
+              for (int r = 0; r < G::RY; ++r) {
+                const int s = G::RB ? (s0 ^ ((r * G::RSTEP) & 1)) : s0;
+                const int lx = 2 * lane + s;
+                const int ly = ly0 + r * G::RSTEP;
+                const bool v = ly < ly_hi && lx >= lx_lo && lx < lx_hi && gxl + s >= 1 &&
+                               gxl + s <= (int)p.nx;
+                vmask |= (unsigned)v << r;
               }
-              const double out = acc_finish<FORM, UNIT, DIV>(acc, uc, fc, p);
-              if (valid) {
-                bad |= !finite64(out);
-                sl_c[rb + xo.c] = out;
-              }
+              const int rb = (ly0 - 1) * G::ROWW + lane;
+              auto rowoff = [&](int d, int k) -> int {
+                return (d == 0 ? um : (d == 1 ? uc : up)) + rb + k * G::ROWW;
+              };
+              const int frow0 = fo + ly0 * G::ROWW + lane;
+              auto foff = [&](int r) -> int { return frow0 + r * G::RSTEP * G::ROWW; };
+              if (s0)
+                bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, 1>(
+                    sm, rowoff, foff, vmask, p);
+              else
+                bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, 0>(
+                    sm, rowoff, foff, vmask, p);
             }
             __syncthreads();
           }(),
@@ -247,22 +286,20 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
     }(std::make_integer_sequence<int, G::K>{});
 
     // ---- finished plane of the owned box -> dst ----
-    const int64_t gz_out = t - G::LAGMAX;
+    const int gz_out = t - G::LAGMAX;
     if (gz_out >= z0 && gz_out < z1) {
-      const double *slot = sm + slot_of(gz_out) * G::SLOT;
+      const int so = uslot(gz_out);
 #pragma unroll
       for (int k = 0; k < G::LPT; ++k) {
         const int pair = tid + k * G::NT;
         const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
         const int lx = 2 * i;
         if (row >= G::GY && row < G::GY + TYo && lx >= G::GX && lx < G::GX + TXo) {
-          const int64_t g = gz_out * p.sz + (gy0 + row) * p.sy + gx0 + lx;
-          stg2(dst + g, slot[row * G::ROWW + 1 + i], slot[row * G::ROWW + G::HW + 1 + i]);
+          const int64_t g = (int64_t)gz_out * p.sz + (int64_t)(gy0 + row) * p.sy + gx0 + lx;
+          stg2(dst + g, sm[so + row * G::ROWW + 1 + i], sm[so + row * G::ROWW + G::HW + 1 + i]);
         }
       }
     }
-    if (do_pf) store_regs(gz_pf, pf);
-    __syncthreads();
   }
   if (bad) atomicOr(p.status, 1);
 }
@@ -275,62 +312,62 @@ __global__ void __launch_bounds__(256, 2)
 k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, Tiles tl) {
   using G = Geo2<S, M>;
   constexpr FPlan P = G::P;
-  constexpr int NNZ = shape_nnz(S);
   extern __shared__ double sm[];
 
-  const int64_t Sx = p.nx + 2, Sy = p.ny + 2;
-  const int64_t item = blockIdx.x;
-  const int64_t tx = item % tl.ntx;
-  const int64_t yc = item / tl.ntx;
-  const int64_t x0 = tile_start(tx, Sx, tl.ntx), x1 = tile_start(tx + 1, Sx, tl.ntx);
-  const int64_t y0 = chunk_start(yc, Sy, tl.nty), y1 = chunk_start(yc + 1, Sy, tl.nty);
-  const int TXo = (int)(x1 - x0);
-  const int64_t gx0 = x0 - G::GX;
-  const int64_t yb = y0 - G::GY;  // first row of block 0
+  const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2;
+  const int item = blockIdx.x;
+  const int tx = item % (int)tl.ntx;
+  const int yc = item / (int)tl.ntx;
+  const int x0 = (int)tile_start(tx, Sx, tl.ntx), x1 = (int)tile_start(tx + 1, Sx, tl.ntx);
+  const int y0 = (int)chunk_start(yc, Sy, tl.nty), y1 = (int)chunk_start(yc + 1, Sy, tl.nty);
+  const int TXo = x1 - x0;
+  const int gx0 = x0 - G::GX;
+  const int yb = y0 - G::GY;  // first row of block 0
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int base_par = (int)((gx0 - 1 + p.px) & 1);
+  const int base_par = (gx0 - 1 + p.px) & 1;
 
-  auto srow = [](int64_t gy, int64_t yb_) -> int { return (int)((gy - yb_) % G::WR); };
+  // rows are >= yb - 1 whenever they are touched
+  auto urow = [&](int gy) -> int { return ((gy - yb + G::WR) % G::WR) * G::ROWW; };
+  auto frow = [&](int gy) -> int { return G::FOFF + ((gy - yb + G::WRF) % G::WRF) * G::ROWW; };
 
-  auto load_regs = [&](int64_t blk, double2 (&r)[G::LPT]) {
+  auto load_regs = [&](const double *base, int blk, int ylim, double2 (&r)[G::LPT]) {
 #pragma unroll
     for (int k = 0; k < G::LPT; ++k) {
       const int pair = tid + k * G::NT;
       const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      const int64_t gx = gx0 + 2 * i, gy = yb + blk * G::R + row;
-      const bool ok = gy >= 0 && gy < Sy && gy < y1 + G::GY && gx >= 0 && gx < Sx;
-      r[k] = ok ? ldg_nc2(src + gy * p.sy + gx) : make_double2(0.0, 0.0);
+      const int gx = gx0 + 2 * i, gy = yb + blk * G::R + row;
+      const bool ok = gy >= 0 && gy < Sy && gy < ylim && gx >= 0 && gx < Sx;
+      r[k] = ok ? ldg_nc2(base + (int64_t)gy * p.sy + gx) : make_double2(0.0, 0.0);
     }
   };
-  auto store_regs = [&](int64_t blk, const double2 (&r)[G::LPT]) {
+  auto store_regs = [&](bool is_f, int blk, const double2 (&r)[G::LPT]) {
 #pragma unroll
     for (int k = 0; k < G::LPT; ++k) {
       const int pair = tid + k * G::NT;
       const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      double *rp = sm + srow(yb + blk * G::R + row, yb) * G::ROWW;
-      rp[1 + i] = r[k].x;
-      rp[G::HW + 1 + i] = r[k].y;
+      const int gy = yb + blk * G::R + row;
+      const int off = is_f ? frow(gy) : urow(gy);
+      sm[off + 1 + i] = r[k].x;
+      sm[off + G::HW + 1 + i] = r[k].y;
     }
   };
 
-  // last step: the block whose output window contains row y1-1
-  const int64_t T_end = (y1 - 1 + G::LAGMAX - yb) / G::R;
-  {
-    double2 r[G::LPT];
-    load_regs(0, r);
-    store_regs(0, r);
-    load_regs(1, r);
-    store_regs(1, r);
-  }
-  __syncthreads();
+  const int ylim = y1 + G::GY;
+  const int T_end = (y1 - 1 + G::LAGMAX - yb) / G::R;
+  double2 pu[G::LPT], pf[G::LPT];
+  load_regs(src, 0, ylim, pu);
+  store_regs(false, 0, pu);
+  load_regs(src, 1, ylim, pu);
+  if (FORM == 1) load_regs(p.f, 0, ylim, pf);
 
   int bad = 0;
-  for (int64_t T = 0; T <= T_end; ++T) {
-    double2 pf[G::LPT];
-    const int64_t blk_pf = T + 2;
-    const bool do_pf = yb + blk_pf * G::R < y1 + G::GY;
-    if (do_pf) load_regs(blk_pf, pf);
-    const int64_t front = yb + T * G::R;
+  for (int T = 0; T <= T_end; ++T) {
+    store_regs(false, T + 1, pu);
+    if (FORM == 1) store_regs(true, T, pf);
+    __syncthreads();
+    if (yb + (T + 2) * G::R < ylim) load_regs(src, T + 2, ylim, pu);
+    if (FORM == 1 && yb + (T + 1) * G::R < ylim) load_regs(p.f, T + 1, ylim, pf);
+    const int front = yb + T * G::R;
 
     [&]<int... Js>(std::integer_sequence<int, Js...>) {
       (
@@ -338,48 +375,48 @@ k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
             constexpr int J = Js;
             constexpr int c = P.colour[J];
             constexpr int nx_ = P.need[J][0], ny_ = P.need[J][1];
-            int64_t r_lo = front - P.lag[J], r_hi = r_lo + G::R;  // [lo, hi)
+            int r_lo = front - P.lag[J], r_hi = r_lo + G::R;  // [lo, hi)
             if (r_lo < 1) r_lo = 1;
             if (r_lo < y0 - ny_) r_lo = y0 - ny_;
-            if (r_hi > p.ny + 1) r_hi = p.ny + 1;
+            if (r_hi > (int)p.ny + 1) r_hi = (int)p.ny + 1;
             if (r_hi > y1 + ny_) r_hi = y1 + ny_;
             if (r_lo >= r_hi) return;
-            int rstep = 1;
-            if (G::C != 2) {
-              rstep = 2;
-              if ((int)((r_lo - 1 + p.py) & 1) != ((c >> 1) & 1)) ++r_lo;
-            }
-            const int nrows = r_lo < r_hi ? (int)((r_hi - r_lo + rstep - 1) / rstep) : 0;
+            if (!G::RB && (((r_lo - 1 + p.py) & 1) != ((c >> 1) & 1))) ++r_lo;
+            const int npr = r_hi > r_lo ? (r_hi - r_lo + G::RSTEP - 1) / G::RSTEP : 0;
+            const int ngrp = (npr + G::RY - 1) / G::RY;
             const int lx_lo = G::GX - nx_, lx_hi = G::GX + TXo + nx_;
-            for (int it = warp; it < nrows * G::NSTRIP; it += G::NW) {
+            for (int it = warp; it < ngrp * G::NSTRIP; it += G::NW) {
               const int strip = it % G::NSTRIP;
-              const int64_t gy = r_lo + (int64_t)(it / G::NSTRIP) * rstep;
-              const int qy = (int)((gy - 1 + p.py) & 1);
-              const int qxt = G::C == 2 ? ((c + qy) & 1) : (c & 1);
-              const int s = (qxt ^ base_par) & 1;
-              const int li = strip * 32 + lane;  // pair index in the row
-              const int lx = 2 * li + s;
-              const int64_t gx = gx0 + lx;
-              const bool valid = lx >= lx_lo && lx < lx_hi && gx >= 1 && gx <= p.nx;
-              double fc = 0.0;
-              if (FORM == 1 && valid) fc = ldg_nc(p.f + gy * p.sy + gx);
-              const XOff<G::HW> xo(s);
-              double *rc = sm + srow(gy, yb) * G::ROWW + li;
-              const double *rm = sm + srow(gy - 1, yb) * G::ROWW + li;
-              const double *rp = sm + srow(gy + 1, yb) * G::ROWW + li;
-              const double uc = rc[xo.c];
-              double acc = acc_init<FORM, UNIT>(uc, p);
+              const int gy0r = r_lo + (it / G::NSTRIP) * G::RY * G::RSTEP;
+              const int qy = (gy0r - 1 + p.py) & 1;
+              const int qxt = G::RB ? ((c + qy) & 1) : (c & 1);
+              const int s0 = (qxt ^ base_par) & 1;
+              const int li = strip * 32 + lane;
+              const int gxl = gx0 + 2 * li;
+              unsigned vmask = 0;
 #pragma unroll
-              for (int q = 0; q < NNZ; ++q) {
-                const Off o = shape_off(S, q);
-                const double *rr = o.y < 0 ? rm : (o.y > 0 ? rp : rc);
-                acc = acc_add<FORM, UNIT>(acc, rr[xo.at(o.x)], q, p);
+              for (int r = 0; r < G::RY; ++r) {
+                const int s = G::RB ? (s0 ^ ((r * G::RSTEP) & 1)) : s0;
+                const int lx = 2 * li + s;
+                const bool v = gy0r + r * G::RSTEP < r_hi && lx >= lx_lo && lx < lx_hi &&
+                               gxl + s >= 1 && gxl + s <= (int)p.nx;
+                vmask |= (unsigned)v << r;
               }
-              const double out = acc_finish<FORM, UNIT, DIV>(acc, uc, fc, p);
-              if (valid) {
-                bad |= !finite64(out);
-                rc[xo.c] = out;
-              }
+              constexpr int NR = (G::RY - 1) * G::RSTEP + 3;
+              int ro[NR];
+#pragma unroll
+              for (int k = 0; k < NR; ++k) ro[k] = urow(gy0r - 1 + k) + li;
+              auto rowoff = [&](int, int k) -> int { return ro[k]; };
+              int fr[G::RY];
+#pragma unroll
+              for (int r = 0; r < G::RY; ++r) fr[r] = frow(gy0r + r * G::RSTEP) + li;
+              auto foff = [&](int r) -> int { return fr[r]; };
+              if (s0)
+                bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, 1>(
+                    sm, rowoff, foff, vmask, p);
+              else
+                bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, 0>(
+                    sm, rowoff, foff, vmask, p);
             }
             __syncthreads();
           }(),
@@ -391,15 +428,13 @@ k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
     for (int k = 0; k < G::LPT; ++k) {
       const int pair = tid + k * G::NT;
       const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      const int64_t gy = front - G::LAGMAX + row;
+      const int gy = front - G::LAGMAX + row;
       const int lx = 2 * i;
       if (gy >= y0 && gy < y1 && lx >= G::GX && lx < G::GX + TXo) {
-        const double *rp = sm + srow(gy, yb) * G::ROWW;
-        stg2(dst + gy * p.sy + gx0 + lx, rp[1 + i], rp[G::HW + 1 + i]);
+        const int ro = urow(gy);
+        stg2(dst + (int64_t)gy * p.sy + gx0 + lx, sm[ro + 1 + i], sm[ro + G::HW + 1 + i]);
       }
     }
-    if (do_pf) store_regs(blk_pf, pf);
-    __syncthreads();
   }
   if (bad) atomicOr(p.status, 1);
 }
@@ -407,11 +442,39 @@ k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
 // ---------------------------------------------------------------------------
 // host side
 
+// K2 is instantiated only for the natural (shape, colours, weights) combos
+// of the reference kinds and Q1; anything else runs the per-colour path.
+static bool natural_key(const KernelKey &k) {
+  switch (k.shape) {
+    case FD5: return k.unit && k.div == DIV_POW2;
+    case FD7: return k.unit && k.div == DIV_RCP;
+    case FE9: return !k.unit && k.div == DIV_RCP;
+    case FE27: return k.unit && k.div == DIV_RCP;
+    case Q1: return !k.unit && k.div == DIV_RCP;
+  }
+  return false;
+}
+
+template <typename Fn>
+static cudaError_t dispatch_fused(const KernelKey &k, Fn &&fn) {
+  const bool d = k.form == 1;
+  switch (k.shape) {
+    case FD5: return d ? fn.template operator()<FD5, 1, true, DIV_POW2>() : fn.template operator()<FD5, 0, true, DIV_POW2>();
+    case FD7: return d ? fn.template operator()<FD7, 1, true, DIV_RCP>() : fn.template operator()<FD7, 0, true, DIV_RCP>();
+    case FE9: return d ? fn.template operator()<FE9, 1, false, DIV_RCP>() : fn.template operator()<FE9, 0, false, DIV_RCP>();
+    case FE27: return d ? fn.template operator()<FE27, 1, true, DIV_RCP>() : fn.template operator()<FE27, 0, true, DIV_RCP>();
+    case Q1: return d ? fn.template operator()<Q1, 1, false, DIV_RCP>() : fn.template operator()<Q1, 0, false, DIV_RCP>();
+  }
+  return cudaErrorInvalidValue;
+}
+
 static bool fused_supported(const KernelKey &key, const Params &p) {
-  if (p.batch != 1) return false;
+  if (p.batch != 1 || !natural_key(key)) return false;
   if (p.colours != natural_colours(key.shape)) return false;
-  const int64_t Sx = p.nx + 2;
+  const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
   if (Sx & 1) return false;  // 16-byte row alignment
+  if (Sx * Sy * (shape_dim(key.shape) == 3 ? Sz : 1) >= (int64_t(1) << 40)) return false;
+  if (Sx > (1 << 20) || Sy > (1 << 20) || Sz > (1 << 20)) return false;  // 32-bit tile maths
   if (((uintptr_t)p.u & 15) || (p.f && ((uintptr_t)p.f & 15))) return false;
   return true;
 }
@@ -442,18 +505,18 @@ static int64_t pick_chunks(int64_t cols, int64_t len, int64_t slots, int64_t ext
 
 template <typename Kern>
 static cudaError_t prepare(Kern kern, size_t smem, int threads, int64_t *slots) {
-  static thread_local int cached_dev = -1;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
   int occ = 0, sms = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  cached_dev = dev;
   *slots = (int64_t)(occ > 0 ? occ : 1) * sms;
   return cudaSuccess;
 }
@@ -509,13 +572,14 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
   int cur = 0;
   cudaError_t e = cudaSuccess;
   for (int s = 0; s < sweeps && e == cudaSuccess; ++s) {
-    e = dispatch(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
+    e = dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
       return launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
     });
     cur ^= 1;
   }
   if (e == cudaSuccess && cur == 1) {
     e = cudaMemcpyAsync(p.u, workspace, need, cudaMemcpyDeviceToDevice, st);
+    note_launch();
   }
   return e;
 }
