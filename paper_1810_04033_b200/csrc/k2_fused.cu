@@ -24,6 +24,7 @@
 // so the result is bitwise identical to the per-colour path and the oracle.
 #include "k2_fused.cuh"
 #include "plan.cuh"
+#include "k2_strip2d.cuh"
 
 #include <utility>
 
@@ -71,8 +72,8 @@ struct Geo3 {
   static constexpr int PY = 32;
   static constexpr int TX = PX - 2 * GX;
   static constexpr int TY = PY - 2 * GY;
-  static constexpr int W = LAGMAX + 3;       // u plane slots
-  static constexpr int WF = LAGMAX + 1;      // f plane slots
+  static constexpr int W = 4;                // u plane slots (>= LAGMAX + 3, power of 2)
+  static constexpr int WF = 2;               // f plane slots (>= LAGMAX + 1, power of 2)
   static constexpr int SLOT = PY * ROWW;
   static constexpr int RSTEP = RB ? 1 : 2;   // point rows of one colour
   static constexpr int RY = RB ? 4 : 2;      // point rows per warp item
@@ -82,11 +83,11 @@ struct Geo3 {
   static constexpr int NW = NT / 32;
   static constexpr int PAIRS = PY * PX / 2;
   static constexpr int LPT = PAIRS / NT;
-  static constexpr int UOFF = 0;
   static constexpr int FOFF = W * SLOT;
   static constexpr size_t SMEM = size_t((W + WF) * SLOT + PAD_ROWS * ROWW) * sizeof(double);
   static_assert(PAIRS % NT == 0, "plane load split");
   static_assert(TX >= 8 && TY >= 4, "ghost margin too wide for the tile");
+  static_assert(W >= LAGMAX + 3 && WF >= LAGMAX + 1, "window too short for the lag");
 };
 
 template <int S, int M>
@@ -101,13 +102,11 @@ struct Geo2 {
   static constexpr int HW = PX / 2 + 2;
   static constexpr int ROWW = 2 * HW;
   static constexpr int R = 8;                // rows per macro-step
-  static constexpr int NB = 3;               // u row blocks resident
-  static constexpr int NBF = 2;              // f row blocks resident
-  static constexpr int WR = NB * R;
-  static constexpr int WRF = NBF * R;
+  static constexpr int WR = 32;              // u rows resident (4 blocks, power of 2)
+  static constexpr int WRF = 16;             // f rows resident (2 blocks)
   static constexpr int TX = PX - 2 * GX;
   static constexpr int RSTEP = RB ? 1 : 2;
-  static constexpr int RY = 2;
+  static constexpr int RY = RB ? 4 : 2;
   static constexpr int NT = 256;
   static constexpr int NW = NT / 32;
   static constexpr int PAIRS = R * PX / 2;
@@ -116,6 +115,7 @@ struct Geo2 {
   static constexpr size_t SMEM = size_t((WR + WRF) * ROWW) * sizeof(double);
   static_assert(LAGMAX + 1 <= R, "row block shorter than the phase lag");
   static_assert(PAIRS % NT == 0, "block load split");
+  static_assert(WR >= 3 * R && WRF >= 2 * R, "window too short");
 };
 
 struct Tiles {
@@ -129,44 +129,57 @@ __host__ __device__ constexpr int xoff(int s, int dx) {
   return (((s + dx) & 1) ? HW : 0) + 1 + ((s + dx) >> 1);
 }
 
+// Non-finite detector: exponent field all ones.
+__device__ __forceinline__ unsigned nonfinite_bits(double v) {
+  return ((unsigned)__double2hiint(v) & 0x7ff00000u) == 0x7ff00000u;
+}
+
 // ---------------------------------------------------------------------------
-// one warp item: RY point rows of a 32-lane strip.
-//   rowoff[dz+1][k]: smem element offset of source row k (point row r uses
-//   k = r*RSTEP + dy + 1), lane included.  s0: x parity of row 0's points.
-// All loads happen before any store, so repeated (row, x) loads are CSE'd.
+// one warp item: RY point rows of a 32-lane strip, x parity pattern fixed at
+// compile time (S0 = parity of row 0; red-black rows alternate).
+//   ro(dz, k): smem element offset of source row k of plane dz (point row r
+//   uses k = r*RSTEP + dy + 1), lane included;  fo(r): f offset of point row r.
+// All loads precede all stores, so repeated (row, x) loads are CSE'd.
 
 template <int S, int FORM, bool UNIT, int DIV, int RY, int RSTEP, bool RB, int HW, int S0,
           typename RowOff, typename FOff>
-__device__ __forceinline__ int update_item(double *sm, const RowOff &rowoff, const FOff &foff,
-                                           unsigned vmask, const Params &p) {
+__device__ __forceinline__ unsigned update_item(const RowOff &ro, const FOff &fo, unsigned vmask,
+                                                const Params &p) {
+  extern __shared__ double sm[];
   constexpr int NNZ = shape_nnz(S);
   double out[RY];
 #pragma unroll
   for (int r = 0; r < RY; ++r) {
     const int s = RB ? (S0 ^ ((r * RSTEP) & 1)) : S0;
     const int kc = r * RSTEP + 1;
-    const double uc = sm[rowoff(1, kc) + (s ? xoff<HW>(1, 0) : xoff<HW>(0, 0))];
+    const double uc = sm[ro(1, kc) + xoff<HW>(s, 0)];
     double acc = acc_init<FORM, UNIT>(uc, p);
 #pragma unroll
     for (int q = 0; q < NNZ; ++q) {
       const Off o = shape_off(S, q);
-      const int off = s ? xoff<HW>(1, o.x) : xoff<HW>(0, o.x);
-      acc = acc_add<FORM, UNIT>(acc, sm[rowoff(o.z + 1, kc + o.y) + off], q, p);
+      acc = acc_add<FORM, UNIT>(acc, sm[ro(o.z + 1, kc + o.y) + xoff<HW>(s, o.x)], q, p);
     }
     double fc = 0.0;
-    if (FORM == 1) fc = sm[foff(r) + (s ? xoff<HW>(1, 0) : xoff<HW>(0, 0))];
+    if (FORM == 1) fc = sm[fo(r) + xoff<HW>(s, 0)];
     out[r] = acc_finish<FORM, UNIT, DIV>(acc, uc, fc, p);
   }
-  int bad = 0;
+  unsigned bad = 0;
 #pragma unroll
   for (int r = 0; r < RY; ++r) {
     const int s = RB ? (S0 ^ ((r * RSTEP) & 1)) : S0;
     if (vmask & (1u << r)) {
-      bad |= !finite64(out[r]);
-      sm[rowoff(1, r * RSTEP + 1) + (s ? xoff<HW>(1, 0) : xoff<HW>(0, 0))] = out[r];
+      bad |= nonfinite_bits(out[r]);
+      sm[ro(1, r * RSTEP + 1) + xoff<HW>(s, 0)] = out[r];
     }
   }
   return bad;
+}
+
+// x parity (0 = even local x) of colour c's points in a row/plane with y/z
+// parities qy, qz.  Tiles start at an even global x (origin x parity 0), so
+// local and global x parity agree and q_x = 1 - (x & 1).
+__host__ __device__ constexpr int x_parity(int colours, int c, int qy, int qz) {
+  return 1 ^ (colours == 2 ? ((c + qy + qz) & 1) : (c & 1));
 }
 
 // ---------------------------------------------------------------------------
@@ -180,6 +193,7 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
   extern __shared__ double sm[];
 
   const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2, Sz = (int)p.nz + 2;
+  const int nx = (int)p.nx, ny = (int)p.ny, nz = (int)p.nz;
   const int item = blockIdx.x;
   const int tx = item % (int)tl.ntx;
   const int ty = (item / (int)tl.ntx) % (int)tl.nty;
@@ -190,10 +204,12 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
   const int TXo = x1 - x0, TYo = y1 - y0;
   const int gx0 = x0 - G::GX, gy0 = y0 - G::GY;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int base_par = (gx0 - 1 + p.px) & 1;
 
-  auto uslot = [](int gz) -> int { return ((gz % G::W) + G::W) % G::W * G::SLOT; };
-  auto fslot = [](int gz) -> int { return G::FOFF + ((gz % G::WF) + G::WF) % G::WF * G::SLOT; };
+  // lane validity in x for both parities: local x = 2*lane + s, global gx0 + x
+  auto xok = [&](int s, int need) -> bool {
+    const int lx = 2 * lane + s, gx = gx0 + lx;
+    return lx >= G::GX - need && lx < G::GX + TXo + need && gx >= 1 && gx <= nx;
+  };
 
   auto load_regs = [&](const double *base, int gz, double2 (&r)[G::LPT]) {
 #pragma unroll
@@ -214,21 +230,24 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
       sm[off + row * G::ROWW + G::HW + 1 + i] = r[k].y;
     }
   };
+  auto uslot = [](int gz) -> int { return (gz & (G::W - 1)) * G::SLOT; };
+  auto fslot = [](int gz) -> int { return G::FOFF + (gz & (G::WF - 1)) * G::SLOT; };
 
   const int t_begin = z0 - G::GZ - 1;
   const int t_end = z1 - 1 + G::LAGMAX;
+  const int zlim = z1 + G::GZ;
   double2 pu[G::LPT], pf[G::LPT];
   load_regs(src, t_begin + 1, pu);
   if (FORM == 1) load_regs(p.f, t_begin, pf);
 
-  int bad = 0;
+  unsigned bad = 0;
   for (int t = t_begin; t <= t_end; ++t) {
     // planes loaded during the previous step go into their (free) slots
-    if (t + 1 < z1 + G::GZ) store_regs(uslot(t + 1), pu);
-    if (FORM == 1 && t < z1 + G::GZ) store_regs(fslot(t), pf);
+    if (t + 1 < zlim) store_regs(uslot(t + 1), pu);
+    if (FORM == 1 && t < zlim) store_regs(fslot(t), pf);
     __syncthreads();
-    if (t + 2 < z1 + G::GZ) load_regs(src, t + 2, pu);
-    if (FORM == 1 && t + 1 < z1 + G::GZ) load_regs(p.f, t + 1, pf);
+    if (t + 2 < zlim) load_regs(src, t + 2, pu);
+    if (FORM == 1 && t + 1 < zlim) load_regs(p.f, t + 1, pf);
 
     // ---- colour phases, in order ----
     [&]<int... Js>(std::integer_sequence<int, Js...>) {
@@ -238,47 +257,35 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
             constexpr int c = P.colour[J];
             constexpr int nx_ = P.need[J][0], ny_ = P.need[J][1], nz_ = P.need[J][2];
             const int pz = t - P.lag[J];
-            if (pz < 1 || pz > (int)p.nz || pz < z0 - nz_ || pz >= z1 + nz_) return;
+            if (pz < 1 || pz > nz || pz < z0 - nz_ || pz >= z1 + nz_) return;
             const int qz = (pz - 1 + p.pz) & 1;
             if (!G::RB && ((c >> 2) & 1) != qz) return;
-            int ly_lo = G::GY - ny_, ly_hi = G::GY + TYo + ny_;
+            int ly_lo = G::GY - ny_, ly_hi = G::GY + TYo + ny_;  // [lo, hi) slot rows
             if (gy0 + ly_lo < 1) ly_lo = 1 - gy0;
-            if (gy0 + ly_hi > (int)p.ny + 1) ly_hi = (int)p.ny + 1 - gy0;
-            if (!G::RB && (((gy0 + ly_lo - 1 + p.py) & 1) != ((c >> 1) & 1))) ++ly_lo;
+            if (gy0 + ly_hi > ny + 1) ly_hi = ny + 1 - gy0;
+            // align row 0 of every item to the parity with x parity 0
+            const int want_qy = G::RB ? ((1 + c + qz) & 1) : ((c >> 1) & 1);
+            const int ly_first = ly_lo;
+            if (((gy0 + ly_lo - 1 + p.py) & 1) != want_qy) --ly_lo;
+            constexpr int S0 = G::RB ? 0 : x_parity(G::C, c, (c >> 1) & 1, 0);
             const int npr = ly_hi > ly_lo ? (ly_hi - ly_lo + G::RSTEP - 1) / G::RSTEP : 0;
             const int nitems = (npr + G::RY - 1) / G::RY;
-            const int lx_lo = G::GX - nx_, lx_hi = G::GX + TXo + nx_;
-            const int um = uslot(pz - 1), uc = uslot(pz), up = uslot(pz + 1);
-            const int fo = fslot(pz);
+            const bool ok0 = xok(S0, nx_), ok1 = xok(S0 ^ 1, nx_);
+            const int um = uslot(pz - 1) + lane, uc = uslot(pz) + lane, up = uslot(pz + 1) + lane;
+            const int fo0 = fslot(pz) + lane;
             for (int it = warp; it < nitems; it += G::NW) {
               const int ly0 = ly_lo + it * G::RY * G::RSTEP;
-              const int gy = gy0 + ly0;
-              const int qy = (gy - 1 + p.py) & 1;
-              const int qxt = G::RB ? ((c + qy + qz) & 1) : (c & 1);
-              const int s0 = (qxt ^ base_par) & 1;
-              const int gxl = gx0 + 2 * lane;  // global x of the lane's even column
               unsigned vmask = 0;
 #pragma unroll
               for (int r = 0; r < G::RY; ++r) {
-                const int s = G::RB ? (s0 ^ ((r * G::RSTEP) & 1)) : s0;
-                const int lx = 2 * lane + s;
                 const int ly = ly0 + r * G::RSTEP;
-                const bool v = ly < ly_hi && lx >= lx_lo && lx < lx_hi && gxl + s >= 1 &&
-                               gxl + s <= (int)p.nx;
-                vmask |= (unsigned)v << r;
+                const bool xo = (G::RB && (r & 1)) ? ok1 : ok0;
+                vmask |= (unsigned)(xo && ly >= ly_first && ly < ly_hi) << r;
               }
-              const int rb = (ly0 - 1) * G::ROWW + lane;
-              auto rowoff = [&](int d, int k) -> int {
-                return (d == 0 ? um : (d == 1 ? uc : up)) + rb + k * G::ROWW;
-              };
-              const int frow0 = fo + ly0 * G::ROWW + lane;
-              auto foff = [&](int r) -> int { return frow0 + r * G::RSTEP * G::ROWW; };
-              if (s0)
-                bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, 1>(
-                    sm, rowoff, foff, vmask, p);
-              else
-                bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, 0>(
-                    sm, rowoff, foff, vmask, p);
+              const int rb = (ly0 - 1) * G::ROWW;
+              auto ro = [&](int d, int k) -> int { return (d == 0 ? um : (d == 1 ? uc : up)) + rb + k * G::ROWW; };
+              auto fo = [&](int r) -> int { return fo0 + (ly0 + r * G::RSTEP) * G::ROWW; };
+              bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, S0>(ro, fo, vmask, p);
             }
             __syncthreads();
           }(),
@@ -315,6 +322,7 @@ k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
   extern __shared__ double sm[];
 
   const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2;
+  const int nx = (int)p.nx, ny = (int)p.ny;
   const int item = blockIdx.x;
   const int tx = item % (int)tl.ntx;
   const int yc = item / (int)tl.ntx;
@@ -322,13 +330,11 @@ k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
   const int y0 = (int)chunk_start(yc, Sy, tl.nty), y1 = (int)chunk_start(yc + 1, Sy, tl.nty);
   const int TXo = x1 - x0;
   const int gx0 = x0 - G::GX;
-  const int yb = y0 - G::GY;  // first row of block 0
+  const int yb = y0 - G::GY;  // first row of block 0; rows touched are >= yb - 1
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int base_par = (gx0 - 1 + p.px) & 1;
 
-  // rows are >= yb - 1 whenever they are touched
-  auto urow = [&](int gy) -> int { return ((gy - yb + G::WR) % G::WR) * G::ROWW; };
-  auto frow = [&](int gy) -> int { return G::FOFF + ((gy - yb + G::WRF) % G::WRF) * G::ROWW; };
+  auto urow = [&](int gy) -> int { return ((gy - yb + G::WR) & (G::WR - 1)) * G::ROWW; };
+  auto frow = [&](int gy) -> int { return G::FOFF + ((gy - yb) & (G::WRF - 1)) * G::ROWW; };
 
   auto load_regs = [&](const double *base, int blk, int ylim, double2 (&r)[G::LPT]) {
 #pragma unroll
@@ -360,7 +366,7 @@ k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
   load_regs(src, 1, ylim, pu);
   if (FORM == 1) load_regs(p.f, 0, ylim, pf);
 
-  int bad = 0;
+  unsigned bad = 0;
   for (int T = 0; T <= T_end; ++T) {
     store_regs(false, T + 1, pu);
     if (FORM == 1) store_regs(true, T, pf);
@@ -378,45 +384,41 @@ k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
             int r_lo = front - P.lag[J], r_hi = r_lo + G::R;  // [lo, hi)
             if (r_lo < 1) r_lo = 1;
             if (r_lo < y0 - ny_) r_lo = y0 - ny_;
-            if (r_hi > (int)p.ny + 1) r_hi = (int)p.ny + 1;
+            if (r_hi > ny + 1) r_hi = ny + 1;
             if (r_hi > y1 + ny_) r_hi = y1 + ny_;
             if (r_lo >= r_hi) return;
-            if (!G::RB && (((r_lo - 1 + p.py) & 1) != ((c >> 1) & 1))) ++r_lo;
-            const int npr = r_hi > r_lo ? (r_hi - r_lo + G::RSTEP - 1) / G::RSTEP : 0;
+            const int r_first = r_lo;
+            const int want_qy = G::RB ? ((1 + c) & 1) : ((c >> 1) & 1);
+            if (((r_lo - 1 + p.py) & 1) != want_qy) --r_lo;
+            constexpr int S0 = G::RB ? 0 : x_parity(G::C, c, (c >> 1) & 1, 0);
+            const int npr = (r_hi - r_lo + G::RSTEP - 1) / G::RSTEP;
             const int ngrp = (npr + G::RY - 1) / G::RY;
             const int lx_lo = G::GX - nx_, lx_hi = G::GX + TXo + nx_;
             for (int it = warp; it < ngrp * G::NSTRIP; it += G::NW) {
-              const int strip = it % G::NSTRIP;
-              const int gy0r = r_lo + (it / G::NSTRIP) * G::RY * G::RSTEP;
-              const int qy = (gy0r - 1 + p.py) & 1;
-              const int qxt = G::RB ? ((c + qy) & 1) : (c & 1);
-              const int s0 = (qxt ^ base_par) & 1;
+              const int strip = it & (G::NSTRIP - 1);
+              const int row0 = r_lo + (it / G::NSTRIP) * G::RY * G::RSTEP;
               const int li = strip * 32 + lane;
               const int gxl = gx0 + 2 * li;
               unsigned vmask = 0;
 #pragma unroll
               for (int r = 0; r < G::RY; ++r) {
-                const int s = G::RB ? (s0 ^ ((r * G::RSTEP) & 1)) : s0;
+                const int s = G::RB ? (S0 ^ ((r * G::RSTEP) & 1)) : S0;
                 const int lx = 2 * li + s;
-                const bool v = gy0r + r * G::RSTEP < r_hi && lx >= lx_lo && lx < lx_hi &&
-                               gxl + s >= 1 && gxl + s <= (int)p.nx;
+                const int row = row0 + r * G::RSTEP;
+                const bool v = row >= r_first && row < r_hi && lx >= lx_lo && lx < lx_hi &&
+                               gxl + s >= 1 && gxl + s <= nx;
                 vmask |= (unsigned)v << r;
               }
               constexpr int NR = (G::RY - 1) * G::RSTEP + 3;
-              int ro[NR];
+              int rw[NR];
 #pragma unroll
-              for (int k = 0; k < NR; ++k) ro[k] = urow(gy0r - 1 + k) + li;
-              auto rowoff = [&](int, int k) -> int { return ro[k]; };
-              int fr[G::RY];
+              for (int k = 0; k < NR; ++k) rw[k] = urow(row0 - 1 + k) + li;
+              int fw[G::RY];
 #pragma unroll
-              for (int r = 0; r < G::RY; ++r) fr[r] = frow(gy0r + r * G::RSTEP) + li;
-              auto foff = [&](int r) -> int { return fr[r]; };
-              if (s0)
-                bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, 1>(
-                    sm, rowoff, foff, vmask, p);
-              else
-                bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, 0>(
-                    sm, rowoff, foff, vmask, p);
+              for (int r = 0; r < G::RY; ++r) fw[r] = frow(row0 + r * G::RSTEP) + li;
+              auto ro = [&](int, int k) -> int { return rw[k]; };
+              auto fo = [&](int r) -> int { return fw[r]; };
+              bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, S0>(ro, fo, vmask, p);
             }
             __syncthreads();
           }(),
@@ -470,6 +472,7 @@ static cudaError_t dispatch_fused(const KernelKey &k, Fn &&fn) {
 
 static bool fused_supported(const KernelKey &key, const Params &p) {
   if (p.batch != 1 || !natural_key(key)) return false;
+  if (p.px != 0) return false;  // tiles assume even global x at local x = 0
   if (p.colours != natural_colours(key.shape)) return false;
   const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
   if (Sx & 1) return false;  // 16-byte row alignment
@@ -541,20 +544,19 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     note_launch();
     return cudaGetLastError();
   } else {
-    using G = Geo2<S, M>;
-    auto kern = k2_stream2d<S, FORM, UNIT, DIV, M>;
-    static thread_local int64_t slots = 0;
+    using G = GeoS2<S, M>;
+    auto kern = k2_strip2d<S, FORM, UNIT, DIV, M>;
+    static thread_local int64_t slots = 0;  // resident blocks
     if (!slots) {
-      cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
+      cudaError_t e = prepare(kern, 0, 32 * G::WPB, &slots);
       if (e != cudaSuccess) return e;
     }
-    Tiles tl;
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2;
-    tl.ntx = (Sx + G::TX - 1) / G::TX;
-    tl.nty = pick_chunks(tl.ntx, Sy, slots, G::GY + G::LAGMAX + G::R, 2 * G::R);
-    tl.nzc = 1;
-    const int64_t items = tl.ntx * tl.nty;
-    kern<<<(unsigned)items, G::NT, G::SMEM, st>>>(p, src, dst, tl);
+    const int64_t nstrip = (Sx + G::TX - 1) / G::TX;
+    const int64_t nchunk = pick_chunks(nstrip, Sy, slots * G::WPB, G::GY + G::LAGMAX + G::NR, 16);
+    const int64_t warps = nstrip * nchunk;
+    const int64_t blocks = (warps + G::WPB - 1) / G::WPB;
+    kern<<<(unsigned)blocks, 32 * G::WPB, 0, st>>>(p, src, dst, nstrip, nchunk);
     note_launch();
     return cudaGetLastError();
   }
