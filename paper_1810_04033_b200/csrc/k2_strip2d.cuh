@@ -31,6 +31,14 @@ struct GeoS2 {
   static constexpr int NR0 = LAGMAX + 3 + D;
   static constexpr int NR = (NR0 + 1) & ~1;  // even, so slot parity is fixed
   static constexpr int WPB = 4;              // warps per block
+  // does the stencil use offset (dx, dy)?
+  static constexpr bool uses(int dx, int dy) {
+    for (int q = 0; q < shape_nnz(S); ++q) {
+      const Off o = shape_off(S, q);
+      if (o.x == dx && o.y == dy) return true;
+    }
+    return false;
+  }
 };
 
 __device__ __forceinline__ double2 ldg_stream2(const double *p) {
@@ -150,14 +158,15 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
 #pragma unroll
                       for (int dy = 0; dy < 3; ++dy) {
                         const double lo = ulo[RR[dy]], hi = uhi[RR[dy]];
+                        const bool need_l = G::uses(-1, dy - 1), need_r = G::uses(1, dy - 1);
                         if (s == 0) {
-                          v[dy][0] = __shfl_up_sync(0xffffffffu, hi, 1);
+                          v[dy][0] = need_l ? __shfl_up_sync(0xffffffffu, hi, 1) : 0.0;
                           v[dy][1] = lo;
                           v[dy][2] = hi;
                         } else {
                           v[dy][0] = lo;
                           v[dy][1] = hi;
-                          v[dy][2] = __shfl_down_sync(0xffffffffu, lo, 1);
+                          v[dy][2] = need_r ? __shfl_down_sync(0xffffffffu, lo, 1) : 0.0;
                         }
                       }
                       const double uc = v[1][1];
