@@ -548,15 +548,15 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     auto kern = k2_strip2d<S, FORM, UNIT, DIV, M>;
     static thread_local int64_t slots = 0;  // resident blocks
     if (!slots) {
-      cudaError_t e = prepare(kern, 0, 32 * G::WPB, &slots);
+      cudaError_t e = prepare(kern, G::SMEM, 32 * G::WPB, &slots);
       if (e != cudaSuccess) return e;
     }
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2;
     const int64_t nstrip = (Sx + G::TX - 1) / G::TX;
-    const int64_t nchunk = pick_chunks(nstrip, Sy, slots * G::WPB, G::GY + G::LAGMAX + G::NR, 16);
+    const int64_t nchunk = pick_chunks(nstrip, Sy, slots * G::WPB, G::GY + G::LAGMAX + G::U, 16);
     const int64_t warps = nstrip * nchunk;
     const int64_t blocks = (warps + G::WPB - 1) / G::WPB;
-    kern<<<(unsigned)blocks, 32 * G::WPB, 0, st>>>(p, src, dst, nstrip, nchunk);
+    kern<<<(unsigned)blocks, 32 * G::WPB, G::SMEM, st>>>(p, src, dst, nstrip, nchunk);
     note_launch();
     return cudaGetLastError();
   }

@@ -1,19 +1,26 @@
 // k2_strip2d.cuh — K2 for 2D grids: warp-private strip streaming.
 //
 // One warp owns a strip of 64 columns (lane i holds the column pair
-// 2i, 2i+1) and a chunk of rows, and streams the rows through a ring of
-// registers: no shared memory, no block barriers, warps fully independent.
-// The strip overlaps its neighbours by the ghost margin GX on each side, so
-// only TX = 64 - 2*GX columns are owned; x+-1 neighbours of the lane's point
-// come from its own pair or, across the pair boundary, from the adjacent
-// lane by one warp shuffle.
+// 2i, 2i+1) and a chunk of rows, and streams the rows: no block barriers,
+// warps fully independent.  The strip overlaps its neighbours by the ghost
+// margin GX on each side, so TX = 64 - 2*GX columns are owned; x+-1
+// neighbours of the lane's point come from its own pair or, across the pair
+// boundary, from the adjacent lane by one warp shuffle.
+//
+// Memory path: each warp has a private ring of NS row slots in shared
+// memory (u row segment + f row segment, 1 KB).  Lane 0 keeps NS rows in
+// flight with TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx) —
+// one 512-byte copy per array per row, no registers held while in flight.
+// At step t the warp waits on row t+1's mbarrier, moves the lane's pair into
+// a small register ring (rows t-LAGMAX-1 .. t+1) and re-arms the slot for
+// row t+1+NS.
 //
 // Phase k processes row t - lag[k] at step t (plan.cuh).  The step loop is
-// unrolled by the ring length NR with the row parity of every ring slot
-// fixed at compile time, so each phase's colour pattern (which rows hold
-// the colour, which x parity its points have) and every ring index are
-// compile-time: inactive phases vanish, the hot loop is loads, shuffles and
-// fp64 arithmetic.  Rows are prefetched D steps ahead (16-byte LDG per lane).
+// unrolled by U (a multiple of both ring lengths) with the row parity of
+// every slot fixed at compile time, so each phase's colour pattern (which
+// rows hold the colour, which x parity its points have) and every ring index
+// are compile-time: inactive phases vanish; the hot loop is LDS, shuffles
+// and fp64 arithmetic.
 #pragma once
 #include "plan.cuh"
 
@@ -27,10 +34,15 @@ struct GeoS2 {
   static constexpr int GX = (P.load[0] + 1) & ~1;
   static constexpr int GY = P.load[1];
   static constexpr int TX = 64 - 2 * GX;
-  static constexpr int D = 4;  // prefetch distance (rows)
-  static constexpr int NR0 = LAGMAX + 3 + D;
-  static constexpr int NR = (NR0 + 1) & ~1;  // even, so slot parity is fixed
-  static constexpr int WPB = 4;              // warps per block
+  static constexpr int NRR0 = LAGMAX + 3;             // register ring: rows t-LAGMAX-1 .. t+1
+  static constexpr int NRR = NRR0 <= 2 ? 2 : (NRR0 <= 4 ? 4 : 8);
+  static constexpr int NS = 8;                         // smem ring slots (rows in flight)
+  static constexpr int U = NRR > NS ? NRR : NS;        // unroll: multiple of both (powers of 2)
+  static constexpr int WPB = 4;                        // warps per block
+  static constexpr int ROWB = 64 * 8;                  // bytes of one array's row segment
+  static constexpr int SLOTB = 2 * ROWB;               // u + f
+  static constexpr size_t SMEM = size_t(WPB) * NS * SLOTB;
+  static_assert(NRR >= NRR0, "register ring too short");
   // does the stencil use offset (dx, dy)?
   static constexpr bool uses(int dx, int dy) {
     for (int q = 0; q < shape_nnz(S); ++q) {
@@ -41,14 +53,35 @@ struct GeoS2 {
   }
 };
 
-__device__ __forceinline__ double2 ldg_stream2(const double *p) {
-  double2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-  return v;
-}
-
 __device__ __forceinline__ void stg_pair(double *p, double a, double b) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t addr, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(addr), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
 }
 
 // Markstein-corrected division for the hot loop: the fallback runs only for
@@ -73,11 +106,14 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
            int64_t nchunk) {
   using G = GeoS2<S, M>;
   constexpr FPlan P = G::P;
-  constexpr int NR = G::NR;
+  constexpr int NRR = G::NRR, NS = G::NS;
   constexpr int NNZ = shape_nnz(S);
-  const int lane = threadIdx.x & 31;
-  const int64_t wid = (int64_t)blockIdx.x * G::WPB + (threadIdx.x >> 5);
-  if (wid >= nstrip * nchunk) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t mbar[G::WPB][NS];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t wid = (int64_t)blockIdx.x * G::WPB + warp;
+  if (wid >= nstrip * nchunk) return;  // whole warp exits together, before any copy
   const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2;
   const int nx = (int)p.nx, ny = (int)p.ny;
   const int strip = (int)(wid % nstrip), chunk = (int)(wid / nstrip);
@@ -85,17 +121,47 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
   const int x1 = (int)(2 * (((int64_t)(strip + 1) * (Sx / 2)) / nstrip));
   const int y0 = (int)(((int64_t)chunk * Sy) / nchunk), y1 = (int)(((int64_t)(chunk + 1) * Sy) / nchunk);
   const int TXo = x1 - x0;
-  const int gx = x0 - G::GX + 2 * lane;  // global x of the lane's even column
-  const bool in_x = gx >= 0 && gx < Sx;
+  const int gxs = x0 - G::GX;            // global x of the strip's column 0 (even)
+  const int gx = gxs + 2 * lane;         // global x of the lane's even column
   const bool own_x = 2 * lane >= G::GX && 2 * lane < G::GX + TXo;
+  // copy window in x, clipped to the array (16-byte granules)
+  const int cx0 = gxs < 0 ? 0 : gxs;
+  const int cx1 = gxs + 64 > Sx ? Sx : gxs + 64;
+  const uint32_t cbytes = (uint32_t)(cx1 - cx0) * 8u;
+  const uint32_t cdoff = (uint32_t)(cx0 - gxs) * 8u;
 
-  // rows of slot 0 have (row - 1 + py) even
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smraw) + (uint32_t)(warp * NS * G::SLOTB);
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&mbar[warp][0]);
+
+  // rows of register-ring slot 0 have (row - 1 + py) even
   int t_begin = y0 - G::GY - 1;
   if ((t_begin - 1 + p.py) & 1) --t_begin;
   const int t_end = y1 - 1 + G::LAGMAX;
   const int ylim = y1 + G::GY;  // rows >= ylim are never needed
 
-  // per-phase row window and lane validity
+  // lane 0 streams row `row` into smem slot `sl` (row t_begin+1+k lives in slot k % NS)
+  auto issue = [&](int row, int sl) {
+    const uint32_t mb = mb0 + 8u * sl;
+    const bool live = row >= 0 && row < Sy && row < ylim;
+    const uint32_t bytes = live ? (FORM == 1 ? 2u : 1u) * cbytes : 0u;
+    mbar_arrive_tx(mb, bytes);
+    if (live) {
+      const int64_t g = (int64_t)row * p.sy + cx0;
+      const uint32_t d = ring + (uint32_t)sl * G::SLOTB + cdoff;
+      bulk_g2s(d, src + g, cbytes, mb);
+      if (FORM == 1) bulk_g2s(d + G::ROWB, p.f + g, cbytes, mb);
+    }
+  };
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_init(mb0 + 8u * s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < NS; ++k) issue(t_begin + 1 + k, k);
+  }
+  __syncwarp();
+
   int rlo[G::K], rhi[G::K];
 #pragma unroll
   for (int j = 0; j < G::K; ++j) {
@@ -103,36 +169,38 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
     rhi[j] = min(ny, y1 - 1 + P.need[j][1]);
   }
 
-  double ulo[NR], uhi[NR], flo[NR], fhi[NR];
+  double ulo[NRR], uhi[NRR], flo[NRR], fhi[NRR];
 #pragma unroll
-  for (int k = 0; k < NR; ++k) ulo[k] = uhi[k] = flo[k] = fhi[k] = 0.0;
-
-  auto load_row = [&](int row, double &lo, double &hi, double &fl, double &fh) {
-    if (row >= 0 && row < Sy && row < ylim && in_x) {
-      const int64_t g = (int64_t)row * p.sy + gx;
-      const double2 u = ldg_stream2(src + g);
-      lo = u.x;
-      hi = u.y;
-      if (FORM == 1) {
-        const double2 f = ldg_stream2(p.f + g);
-        fl = f.x;
-        fh = f.y;
-      }
-    }
-  };
-#pragma unroll
-  for (int k = 1; k <= G::D; ++k) load_row(t_begin + k, ulo[k], uhi[k], flo[k], fhi[k]);
+  for (int k = 0; k < NRR; ++k) ulo[k] = uhi[k] = flo[k] = fhi[k] = 0.0;
 
   unsigned bad = 0;
-  for (int t0 = t_begin; t0 <= t_end; t0 += NR) {
+  uint32_t round = 0;  // completed passes over the smem ring
+  for (int t0 = t_begin; t0 <= t_end; t0 += G::U, round += G::U / NS) {
     [&]<int... Ks>(std::integer_sequence<int, Ks...>) {
       (
           [&] {
-            constexpr int KS = Ks;  // ring slot of row t
+            constexpr int KS = Ks;  // t - t_begin (mod U)
             const int t = t0 + KS;
+            // ---- row t+1: smem slot -> register ring, re-arm the slot ----
             {
-              constexpr int L = (KS + G::D + 1) % NR;
-              load_row(t + G::D + 1, ulo[L], uhi[L], flo[L], fhi[L]);
+              constexpr int SL = KS % NS;
+              constexpr int RR = (KS + 1) % NRR;
+              mbar_wait(mb0 + 8u * SL, (round + (uint32_t)(KS / NS)) & 1u);
+              const uint32_t a = ring + SL * G::SLOTB + lane * 16u;
+              double2 u2, f2;
+              asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(u2.x), "=d"(u2.y) : "r"(a) : "memory");
+              ulo[RR] = u2.x;
+              uhi[RR] = u2.y;
+              if (FORM == 1) {
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(f2.x), "=d"(f2.y) : "r"(a + G::ROWB) : "memory");
+                flo[RR] = f2.x;
+                fhi[RR] = f2.y;
+              }
+              __syncwarp();
+              if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(t + 1 + NS, SL);
+              }
             }
             // ---- phases in order ----
             [&]<int... Js>(std::integer_sequence<int, Js...>) {
@@ -140,8 +208,8 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                   [&] {
                     constexpr int J = Js;
                     constexpr int c = P.colour[J];
-                    constexpr int R0 = ((KS - P.lag[J]) % NR + NR) % NR;
-                    constexpr int RM = (R0 + NR - 1) % NR, RP = (R0 + 1) % NR;
+                    constexpr int R0 = ((KS - P.lag[J]) % NRR + NRR) % NRR;
+                    constexpr int RM = (R0 + NRR - 1) % NRR, RP = (R0 + 1) % NRR;
                     constexpr int qy = (KS - P.lag[J]) & 1;  // parity of the row being updated
                     if constexpr (!G::RB && qy != ((c >> 1) & 1)) {
                       return;  // colour absent from this row
@@ -152,12 +220,11 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                       const int lx = 2 * lane + s;
                       const bool valid = lx >= G::GX - P.need[J][0] && lx < G::GX + TXo + P.need[J][0] &&
                                          gx + s >= 1 && gx + s <= nx;
-                      // neighbour values v[dy+1][dx+1]
                       double v[3][3];
-                      constexpr int RR[3] = {RM, R0, RP};
+                      constexpr int RRW[3] = {RM, R0, RP};
 #pragma unroll
                       for (int dy = 0; dy < 3; ++dy) {
-                        const double lo = ulo[RR[dy]], hi = uhi[RR[dy]];
+                        const double lo = ulo[RRW[dy]], hi = uhi[RRW[dy]];
                         const bool need_l = G::uses(-1, dy - 1), need_r = G::uses(1, dy - 1);
                         if (s == 0) {
                           v[dy][0] = need_l ? __shfl_up_sync(0xffffffffu, hi, 1) : 0.0;
@@ -197,15 +264,21 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
             }(std::make_integer_sequence<int, G::K>{});
             // ---- row t - LAGMAX is final ----
             {
-              constexpr int RO = ((KS - G::LAGMAX) % NR + NR) % NR;
+              constexpr int RO = ((KS - G::LAGMAX) % NRR + NRR) % NRR;
               const int row = t - G::LAGMAX;
               if (row >= y0 && row < y1 && own_x)
                 stg_pair(dst + (int64_t)row * p.sy + gx, ulo[RO], uhi[RO]);
             }
           }(),
           ...);
-    }(std::make_integer_sequence<int, NR>{});
+    }(std::make_integer_sequence<int, G::U>{});
   }
+  // drain: the NS rows still in flight (one per slot) must land before exit
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_wait(mb0 + 8u * s, round & 1u);
+  }
+  __syncwarp();
   if (bad) atomicOr(p.status, 1);
 }
 
