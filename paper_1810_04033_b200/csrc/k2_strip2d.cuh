@@ -1,16 +1,16 @@
 // k2_strip2d.cuh — K2 for 2D grids: warp-private strip streaming.
 //
-// One warp owns a strip of 64 columns (lane i holds the column pair
-// 2i, 2i+1) and a chunk of rows, and streams the rows: no block barriers,
+// One warp owns a strip of 64*NP columns (lane i holds the NP column pairs
+// 2*NP*i .. 2*NP*i + 2*NP - 1) and a chunk of rows, and streams the rows: no block barriers,
 // warps fully independent.  The strip overlaps its neighbours by the ghost
 // margin GX on each side, so TX = 64 - 2*GX columns are owned; x+-1
 // neighbours of the lane's point come from its own pair or, across the pair
 // boundary, from the adjacent lane by one warp shuffle.
 //
 // Memory path: each warp has a private ring of NS row slots in shared
-// memory (u row segment + f row segment, 1 KB).  Lane 0 keeps NS rows in
+// memory (u row segment + f row segment).  Lane 0 keeps NS rows in
 // flight with TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx) —
-// one 512-byte copy per array per row, no registers held while in flight.
+// one copy per array per row, no registers held while in flight.
 // At step t the warp waits on row t+1's mbarrier, moves the lane's pair into
 // a small register ring (rows t-LAGMAX-1 .. t+1) and re-arms the slot for
 // row t+1+NS.
@@ -33,13 +33,15 @@ struct GeoS2 {
   static constexpr bool RB = (P.C == 2);
   static constexpr int GX = (P.load[0] + 1) & ~1;
   static constexpr int GY = P.load[1];
-  static constexpr int TX = 64 - 2 * GX;
+  static constexpr int NP = 2;                         // column pairs per lane
+  static constexpr int WS = 64 * NP;                   // strip width (columns)
+  static constexpr int TX = WS - 2 * GX;
   static constexpr int NRR0 = LAGMAX + 3;             // register ring: rows t-LAGMAX-1 .. t+1
   static constexpr int NRR = NRR0 <= 2 ? 2 : (NRR0 <= 4 ? 4 : 8);
   static constexpr int NS = 8;                         // smem ring slots (rows in flight)
   static constexpr int U = NRR > NS ? NRR : NS;        // unroll: multiple of both (powers of 2)
   static constexpr int WPB = 4;                        // warps per block
-  static constexpr int ROWB = 64 * 8;                  // bytes of one array's row segment
+  static constexpr int ROWB = WS * 8;                  // bytes of one array's row segment
   static constexpr int SLOTB = 2 * ROWB;               // u + f
   static constexpr size_t SMEM = size_t(WPB) * NS * SLOTB;
   static_assert(NRR >= NRR0, "register ring too short");
@@ -121,12 +123,13 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
   const int x1 = (int)(2 * (((int64_t)(strip + 1) * (Sx / 2)) / nstrip));
   const int y0 = (int)(((int64_t)chunk * Sy) / nchunk), y1 = (int)(((int64_t)(chunk + 1) * Sy) / nchunk);
   const int TXo = x1 - x0;
+  constexpr int NP = G::NP, NC = 2 * NP;  // pairs / columns per lane
   const int gxs = x0 - G::GX;            // global x of the strip's column 0 (even)
-  const int gx = gxs + 2 * lane;         // global x of the lane's even column
-  const bool own_x = 2 * lane >= G::GX && 2 * lane < G::GX + TXo;
+  const int lx0 = NC * lane;             // strip-local x of the lane's first column
+  const int gx = gxs + lx0;              // global x of the lane's first column
   // copy window in x, clipped to the array (16-byte granules)
   const int cx0 = gxs < 0 ? 0 : gxs;
-  const int cx1 = gxs + 64 > Sx ? Sx : gxs + 64;
+  const int cx1 = gxs + G::WS > Sx ? Sx : gxs + G::WS;
   const uint32_t cbytes = (uint32_t)(cx1 - cx0) * 8u;
   const uint32_t cdoff = (uint32_t)(cx0 - gxs) * 8u;
 
@@ -169,9 +172,11 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
     rhi[j] = min(ny, y1 - 1 + P.need[j][1]);
   }
 
-  double ulo[NRR], uhi[NRR], flo[NRR], fhi[NRR];
+  double uu[NRR][NC], ff[NRR][NC];
 #pragma unroll
-  for (int k = 0; k < NRR; ++k) ulo[k] = uhi[k] = flo[k] = fhi[k] = 0.0;
+  for (int k = 0; k < NRR; ++k)
+#pragma unroll
+    for (int j = 0; j < NC; ++j) uu[k][j] = ff[k][j] = 0.0;
 
   unsigned bad = 0;
   uint32_t round = 0;  // completed passes over the smem ring
@@ -186,15 +191,14 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
               constexpr int SL = KS % NS;
               constexpr int RR = (KS + 1) % NRR;
               mbar_wait(mb0 + 8u * SL, (round + (uint32_t)(KS / NS)) & 1u);
-              const uint32_t a = ring + SL * G::SLOTB + lane * 16u;
-              double2 u2, f2;
-              asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(u2.x), "=d"(u2.y) : "r"(a) : "memory");
-              ulo[RR] = u2.x;
-              uhi[RR] = u2.y;
-              if (FORM == 1) {
-                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(f2.x), "=d"(f2.y) : "r"(a + G::ROWB) : "memory");
-                flo[RR] = f2.x;
-                fhi[RR] = f2.y;
+              const uint32_t a = ring + SL * G::SLOTB + lane * (NC * 8u);
+#pragma unroll
+              for (int k = 0; k < NP; ++k) {
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                             : "=d"(uu[RR][2 * k]), "=d"(uu[RR][2 * k + 1]) : "r"(a + 16u * k) : "memory");
+                if (FORM == 1)
+                  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                               : "=d"(ff[RR][2 * k]), "=d"(ff[RR][2 * k + 1]) : "r"(a + G::ROWB + 16u * k) : "memory");
               }
               __syncwarp();
               if (lane == 0) {
@@ -217,57 +221,69 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                       constexpr int s = 1 ^ (G::RB ? ((c + qy) & 1) : (c & 1));  // x parity
                       const int row = t - P.lag[J];
                       if (row < rlo[J] || row > rhi[J]) return;
-                      const int lx = 2 * lane + s;
-                      const bool valid = lx >= G::GX - P.need[J][0] && lx < G::GX + TXo + P.need[J][0] &&
-                                         gx + s >= 1 && gx + s <= nx;
-                      double v[3][3];
+                      // the lane's NP points of this colour: local columns 2k + s
+                      double vl[3], vr[3];  // left / right ghost column from the adjacent lanes
                       constexpr int RRW[3] = {RM, R0, RP};
 #pragma unroll
                       for (int dy = 0; dy < 3; ++dy) {
-                        const double lo = ulo[RRW[dy]], hi = uhi[RRW[dy]];
-                        const bool need_l = G::uses(-1, dy - 1), need_r = G::uses(1, dy - 1);
-                        if (s == 0) {
-                          v[dy][0] = need_l ? __shfl_up_sync(0xffffffffu, hi, 1) : 0.0;
-                          v[dy][1] = lo;
-                          v[dy][2] = hi;
+                        if (s == 0 && G::uses(-1, dy - 1))
+                          vl[dy] = __shfl_up_sync(0xffffffffu, uu[RRW[dy]][NC - 1], 1);
+                        if (s == 1 && G::uses(1, dy - 1))
+                          vr[dy] = __shfl_down_sync(0xffffffffu, uu[RRW[dy]][0], 1);
+                      }
+                      double outv[NP];
+                      bool valid[NP];
+#pragma unroll
+                      for (int k = 0; k < NP; ++k) {
+                        const int cc = 2 * k + s;  // lane-local column of the point
+                        const int lx = lx0 + cc;
+                        valid[k] = lx >= G::GX - P.need[J][0] && lx < G::GX + TXo + P.need[J][0] &&
+                                   gx + cc >= 1 && gx + cc <= nx;
+                        auto val = [&](int dy, int dx) -> double {
+                          const int col = cc + dx;
+                          if (col < 0) return vl[dy];
+                          if (col >= NC) return vr[dy];
+                          return uu[RRW[dy]][col];
+                        };
+                        const double uc = uu[R0][cc];
+                        double acc = acc_init<FORM, UNIT>(uc, p);
+#pragma unroll
+                        for (int q = 0; q < NNZ; ++q) {
+                          const Off o = shape_off(S, q);
+                          acc = acc_add<FORM, UNIT>(acc, val(o.y + 1, o.x), q, p);
+                        }
+                        if (FORM == 0) {
+                          outv[k] = div_wc_lane<DIV>(acc, valid[k], p);
                         } else {
-                          v[dy][0] = lo;
-                          v[dy][1] = hi;
-                          v[dy][2] = need_r ? __shfl_down_sync(0xffffffffu, lo, 1) : 0.0;
+                          const double qd = div_wc_lane<DIV>(__dsub_rn(ff[R0][cc], acc), valid[k], p);
+                          outv[k] = __dadd_rn(uc, __dmul_rn(p.omega, qd));
                         }
                       }
-                      const double uc = v[1][1];
-                      double acc = acc_init<FORM, UNIT>(uc, p);
 #pragma unroll
-                      for (int q = 0; q < NNZ; ++q) {
-                        const Off o = shape_off(S, q);
-                        acc = acc_add<FORM, UNIT>(acc, v[o.y + 1][o.x + 1], q, p);
-                      }
-                      double out;
-                      if (FORM == 0) {
-                        out = div_wc_lane<DIV>(acc, valid, p);
-                      } else {
-                        const double fc = s == 0 ? flo[R0] : fhi[R0];
-                        const double qd = div_wc_lane<DIV>(__dsub_rn(fc, acc), valid, p);
-                        out = __dadd_rn(uc, __dmul_rn(p.omega, qd));
-                      }
-                      if (valid) {
-                        bad |= ((unsigned)__double2hiint(out) & 0x7ff00000u) == 0x7ff00000u;
-                        if (s == 0)
-                          ulo[R0] = out;
-                        else
-                          uhi[R0] = out;
-                      }
+                      for (int k = 0; k < NP; ++k)
+                        if (valid[k]) uu[R0][2 * k + s] = outv[k];
                     }
                   }(),
                   ...);
             }(std::make_integer_sequence<int, G::K>{});
-            // ---- row t - LAGMAX is final ----
+            // ---- row t - LAGMAX is final: owned pairs -> dst; non-finite check ----
             {
               constexpr int RO = ((KS - G::LAGMAX) % NRR + NRR) % NRR;
               const int row = t - G::LAGMAX;
-              if (row >= y0 && row < y1 && own_x)
-                stg_pair(dst + (int64_t)row * p.sy + gx, ulo[RO], uhi[RO]);
+              if (row >= y0 && row < y1) {
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                  const int lx = lx0 + 2 * k;
+                  if (lx >= G::GX && lx < G::GX + TXo) {
+                    const double a = uu[RO][2 * k], b = uu[RO][2 * k + 1];
+                    // non-finite results are sticky through later updates, so
+                    // checking each owned value once, when final, catches them
+                    bad |= (((unsigned)__double2hiint(a) & 0x7ff00000u) == 0x7ff00000u) |
+                           (((unsigned)__double2hiint(b) & 0x7ff00000u) == 0x7ff00000u);
+                    stg_pair(dst + (int64_t)row * p.sy + gx + 2 * k, a, b);
+                  }
+                }
+              }
             }
           }(),
           ...);
