@@ -33,14 +33,14 @@ struct GeoS2 {
   static constexpr bool RB = (P.C == 2);
   static constexpr int GX = (P.load[0] + 1) & ~1;
   static constexpr int GY = P.load[1];
-  static constexpr int NP = 2;                         // column pairs per lane
+  static constexpr int NP = 1;                         // column pairs per lane
   static constexpr int WS = 64 * NP;                   // strip width (columns)
   static constexpr int TX = WS - 2 * GX;
   static constexpr int NRR0 = LAGMAX + 3;             // register ring: rows t-LAGMAX-1 .. t+1
   static constexpr int NRR = NRR0 <= 2 ? 2 : (NRR0 <= 4 ? 4 : 8);
   static constexpr int NS = 8;                         // smem ring slots (rows in flight)
   static constexpr int U = NRR > NS ? NRR : NS;        // unroll: multiple of both (powers of 2)
-  static constexpr int WPB = 4;                        // warps per block
+  static constexpr int WPB = 2;                        // warps per block
   static constexpr int ROWB = WS * 8;                  // bytes of one array's row segment
   static constexpr int SLOTB = 2 * ROWB;               // u + f
   static constexpr size_t SMEM = size_t(WPB) * NS * SLOTB;
@@ -96,7 +96,7 @@ __device__ __forceinline__ double div_wc_lane(double a, bool used, const Params 
     const double q0 = __dmul_rn(a, p.rwc);
     const double r = __fma_rn(-p.wc, q0, a);
     double q = __fma_rn(r, p.rwc, q0);
-    if (used && (e - 64u) >= 1918u) q = __ddiv_rn(a, p.wc);  // |a| outside [2^-959, 2^959)
+    if (__builtin_expect(used && (e - 64u) >= 1918u, 0)) q = __ddiv_rn(a, p.wc);  // |a| outside [2^-959, 2^959)
     return q;
   }
   return __ddiv_rn(a, p.wc);
