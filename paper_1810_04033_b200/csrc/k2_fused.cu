@@ -76,8 +76,8 @@ struct Geo3 {
   static constexpr int WF = 2;               // f plane slots (>= LAGMAX + 1, power of 2)
   static constexpr int SLOT = PY * ROWW;
   static constexpr int RSTEP = RB ? 1 : 2;   // point rows of one colour
-  static constexpr int RY = RB ? 4 : 2;      // point rows per warp item
-  static constexpr int MINB = (S == Q1 || S == FE27) ? 1 : 2;  // CTAs/SM (register budget)
+  static constexpr int RY = RB ? 4 : (S == Q1 || S == FE27 ? 1 : 2);  // point rows per warp item
+  static constexpr int MINB = (S == FE27) ? 1 : 2;  // CTAs/SM (register budget)
   static constexpr int PAD_ROWS = (RY - 1) * RSTEP + 2;
   static constexpr int NT = 256;
   static constexpr int NW = NT / 32;
@@ -211,23 +211,32 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
     return lx >= G::GX - need && lx < G::GX + TXo + need && gx >= 1 && gx <= nx;
   };
 
-  auto load_regs = [&](const double *base, int gz, double2 (&r)[G::LPT]) {
+  // per-thread plane coordinates are the same for every plane: precompute
+  // the in-plane global offset, bounds flag, smem offset and ownership once
+  int goff[G::LPT], soff[G::LPT];
+  unsigned inxy = 0, ownm = 0;
 #pragma unroll
-    for (int k = 0; k < G::LPT; ++k) {
-      const int pair = tid + k * G::NT;
-      const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      const int gx = gx0 + 2 * i, gy = gy0 + row;
-      const bool ok = gz >= 0 && gz < Sz && gy >= 0 && gy < Sy && gx >= 0 && gx < Sx;
-      r[k] = ok ? ldg_nc2(base + (int64_t)gz * p.sz + (int64_t)gy * p.sy + gx) : make_double2(0.0, 0.0);
-    }
+  for (int k = 0; k < G::LPT; ++k) {
+    const int pair = tid + k * G::NT;
+    const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
+    const int gx = gx0 + 2 * i, gy = gy0 + row;
+    goff[k] = gy * (int)p.sy + gx;
+    soff[k] = row * G::ROWW + 1 + i;
+    inxy |= (unsigned)(gy >= 0 && gy < Sy && gx >= 0 && gx < Sx) << k;
+    ownm |= (unsigned)(row >= G::GY && row < G::GY + TYo && 2 * i >= G::GX && 2 * i < G::GX + TXo) << k;
+  }
+  auto load_regs = [&](const double *base, int gz, double2 (&r)[G::LPT]) {
+    const bool zok = gz >= 0 && gz < Sz;
+    const double *pb = base + (int64_t)gz * p.sz;
+#pragma unroll
+    for (int k = 0; k < G::LPT; ++k)
+      r[k] = (zok && ((inxy >> k) & 1)) ? ldg_nc2(pb + goff[k]) : make_double2(0.0, 0.0);
   };
   auto store_regs = [&](int off, const double2 (&r)[G::LPT]) {
 #pragma unroll
     for (int k = 0; k < G::LPT; ++k) {
-      const int pair = tid + k * G::NT;
-      const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      sm[off + row * G::ROWW + 1 + i] = r[k].x;
-      sm[off + row * G::ROWW + G::HW + 1 + i] = r[k].y;
+      sm[off + soff[k]] = r[k].x;
+      sm[off + soff[k] + G::HW] = r[k].y;
     }
   };
   auto uslot = [](int gz) -> int { return (gz & (G::W - 1)) * G::SLOT; };
@@ -296,16 +305,10 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
     const int gz_out = t - G::LAGMAX;
     if (gz_out >= z0 && gz_out < z1) {
       const int so = uslot(gz_out);
+      double *pb = dst + (int64_t)gz_out * p.sz;
 #pragma unroll
-      for (int k = 0; k < G::LPT; ++k) {
-        const int pair = tid + k * G::NT;
-        const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-        const int lx = 2 * i;
-        if (row >= G::GY && row < G::GY + TYo && lx >= G::GX && lx < G::GX + TXo) {
-          const int64_t g = (int64_t)gz_out * p.sz + (int64_t)(gy0 + row) * p.sy + gx0 + lx;
-          stg2(dst + g, sm[so + row * G::ROWW + 1 + i], sm[so + row * G::ROWW + G::HW + 1 + i]);
-        }
-      }
+      for (int k = 0; k < G::LPT; ++k)
+        if ((ownm >> k) & 1) stg2(pb + goff[k], sm[so + soff[k]], sm[so + soff[k] + G::HW]);
     }
   }
   if (bad) atomicOr(p.status, 1);
