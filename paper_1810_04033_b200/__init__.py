@@ -10,6 +10,7 @@ from .kernels import (FD5, FD7, FE9, FE27, FE27Q1, STENCILS, CostModel, Numerics
                       ScalarCellKernel, StencilKind, get_stencil, residual_max, update_cell,
                       update_cells_batch)
 from .mesh import Mesh, init, init_rhs, make_mesh
+from .patches import PatchBatch, init_patches
 from .pool import DevicePool, Schedule, WorkerPool
 from .runner import (BenchConfig, BenchResult, ConfigError, StrategyRunner, mesh_digest,
                      parse_cost, run_benchmark)

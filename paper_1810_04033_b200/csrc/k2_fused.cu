@@ -25,6 +25,7 @@
 #include "k2_fused.cuh"
 #include "plan.cuh"
 #include "k2_strip2d.cuh"
+#include "k3_patch.cuh"
 
 #include <utility>
 
@@ -565,9 +566,33 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
   }
 }
 
+// K3: batches of 16x16 FD5 patches, every sweep in one launch, in place
+static bool patch_supported(const KernelKey &key, const Params &p) {
+  return p.batch >= 1 && key.shape == FD5 && key.unit && key.div == DIV_POW2 && p.colours == 2 &&
+         p.nx == 16 && p.ny == 16 && p.px == 0 && p.py == 0;
+}
+
+static cudaError_t launch_patches(const KernelKey &key, const Params &p, int sweeps, cudaStream_t st) {
+  const int64_t threads = p.batch * 32;
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  cudaError_t e = cudaSuccess;
+  if (key.form == 1)
+    k3_patch16_fd5<1, true, DIV_POW2><<<blocks, 256, 0, st>>>(p, sweeps);
+  else
+    k3_patch16_fd5<0, true, DIV_POW2><<<blocks, 256, 0, st>>>(p, sweeps);
+  note_launch();
+  e = cudaGetLastError();
+  return e;
+}
+
 cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, double *workspace,
                          size_t workspace_bytes, cudaStream_t st, int *handled) {
   *handled = 0;
+  if (p.batch > 1 || (p.nx == 16 && p.ny == 16 && shape_dim(key.shape) == 2)) {
+    if (!patch_supported(key, p)) return cudaSuccess;
+    *handled = 1;
+    return launch_patches(key, p, sweeps, st);
+  }
   if (!fused_supported(key, p)) return cudaSuccess;
   const size_t need = fused_workspace_bytes(key, p);
   if (!workspace || workspace_bytes < need || ((uintptr_t)workspace & 15)) return cudaSuccess;
