@@ -259,6 +259,9 @@ def run_ours(args, wl, rank, world, local):
         def step():
             pb.sweep(kind, wl.sweeps, flags=flags)
 
+        def e2e_prep():
+            pass
+
         def e2e_step():
             # the public call a user makes: host patches in, swept patches out
             b = sl.PatchBatch(pinned_u, pinned_f, wl.omega, device=dev)
@@ -275,130 +278,14 @@ def run_ours(args, wl, rank, world, local):
         def step():
             sl.run_sweeps(mesh, kind, cost, wl.sweeps, plan=plan, flags=flags)
 
+        def e2e_prep():
+            mesh.values[:] = u0_host                # host-side prep (untimed)
+
         def e2e_step():
             mesh.set_rhs(f_host, wl.omega)          # f re-uploaded inside the step
             step()                                  # uploads u (H2D), sweeps
             return mesh.values                      # D2H of the result
 
-        def e2e_prep():
-            mesh.values[:] = u0_host                # host-side prep (untimed)
-
-    grid_bytes = wl.grid_elems * 8
-    cfg = {"workload": wl.name, "baseline_config_index": wl.index, "stencil": wl.stencil,
-           "grid": grid, "sweeps_per_step": wl.sweeps, "update": "form D: u += 0.8*(f - A u)/w_c",
-           "seed": wl.seed,
-           "l2": ("flushed between steps (256 MiB write)" if 2 * grid_bytes < 2 * L2_BYTES
-                  else f"inputs larger than L2 ({2 * grid_bytes / 1e9:.2f} GB u+f)"),
-           "parallelism": "single-gpu" if world == 1 else f"replicas x{world}"}
-    if extra:
-        cfg.update(extra)
-    return cfg
-
-
-def cpu_baseline(wl, budget_s=12.0):
-    """Time the C restatement (oracle/, all host threads) on a bounded sample."""
-    import numpy as np
-    from oracle import coracle
-    from oracle import restate as R
-
-    threads = coracle.max_threads()
-    n = wl.n
-    note = "full grid"
-    if wl.dim == 3 and n > 512:
-        n = 512
-        note = "n=512 sub-grid (full 1026^3 u+f would need 17 GB host RAM)"
-    if wl.batch > 1:
-        u, f = R.init_patches(min(wl.batch, 4096), wl.n, wl.seed)
-        note = f"{u.shape[0]} of {wl.batch} patches"
-    else:
-        u = R.init_u(wl.dim, n, wl.seed)
-        f = R.init_f(wl.dim, n, wl.seed + 1)
-    pts = u.size // (n + 2) ** wl.dim * n ** wl.dim
-    t0 = time.perf_counter()
-    coracle.sweep(u, wl.stencil, 1, f=f, omega=wl.omega, form="D", threads=threads)
-    t1 = time.perf_counter()
-    sweeps = 1
-    per = t1 - t0
-    more = max(0, min(wl.sweeps - 1, int(budget_s / max(per, 1e-6)) - 1))
-    if more:
-        coracle.sweep(u, wl.stencil, more, f=f, omega=wl.omega, form="D", threads=threads)
-        sweeps += more
-    t2 = time.perf_counter()
-    del np
-    return {"value": pts * sweeps / (t2 - t0) / 1e9, "unit": UNIT, "cores": threads,
-            "kind": "port",
-            "sample": f"{sweeps} sweep(s) of {wl.stencil} form D on the {note}, "
-                      f"C restatement (oracle/sweep_oracle.c), {threads} pthreads"}
-
-
-def run_reference(args, wl, rank, world):
-    """The reference algorithm on the host cores (C port, all threads)."""
-    if rank != 0:
-        return
-    import numpy as np
-    from oracle import coracle
-    from oracle import restate as R
-
-    threads = coracle.max_threads()
-    n = wl.n
-    note = f"{wl.stencil} full grid"
-    if wl.dim == 3 and n > 512:
-        n = 512
-        note = f"{wl.stencil} n=512 sub-grid of the 1026^3 config"
-    if wl.batch > 1:
-        u, f = R.init_patches(min(wl.batch, 4096), wl.n, wl.seed)
-        note = f"{u.shape[0]} of {wl.batch} patches"
-        pts = u.shape[0] * wl.n ** 2
-    else:
-        u = R.init_u(wl.dim, n, wl.seed)
-        f = R.init_f(wl.dim, n, wl.seed + 1)
-        pts = n ** wl.dim
-    # one step = a bounded sample: as many sweeps as fit ~4 s (>= 1)
-    t0 = time.perf_counter()
-    coracle.sweep(u, wl.stencil, 1, f=f, omega=wl.omega, form="D", threads=threads)
-    per = time.perf_counter() - t0
-    sweeps = max(1, min(wl.sweeps, int(4.0 / max(per, 1e-6))))
-    for _ in range(args.warmup):
-        coracle.sweep(u, wl.stencil, sweeps, f=f, omega=wl.omega, form="D", threads=threads)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        coracle.sweep(u, wl.stencil, sweeps, f=f, omega=wl.omega, form="D", threads=threads)
-        times.append(time.perf_counter() - t0)
-    ms = 1e3 * sum(times) / len(times)
-    value = pts * sweeps / (ms / 1e3) / 1e9
-    sample = f"{sweeps} sweep(s) per step of the {note}, form D, C restatement, {threads} pthreads"
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": workload_config(wl, world, {"parallelism": "host cores"}),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    del np
-    print(json.dumps(line), flush=True)
-
-
-def flush_l2(torch, buf):
-    buf.add_(1.0)
-
-
-def run_ours(args, wl, rank, world, local):
-    import torch
-    import torch.distributed as dist
-
-    import paper_1810_04033_b200 as sl
-    from paper_1810_04033_b200 import _native
-
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    lib = _native.require_cuda()
-    kind = sl.get_stencil(wl.stencil)
-    flags = _native.SL_FLAG_PER_COLOUR if args.per_colour else 0
-
-    if wl.batch > 1:
-        raise SystemExit("config 5 (batched patches) needs the patch runner")
     grid_bytes = wl.grid_elems * 8
     needs_flush = 2 * grid_bytes < 2 * L2_BYTES
     flush_buf = torch.zeros(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev) if needs_flush else None
@@ -440,8 +327,7 @@ def run_ours(args, wl, rank, world, local):
     if not args.no_e2e:
         e2e_times = []
         for i in range(args.steps):
-            if wl.batch == 1:
-                e2e_prep()
+            e2e_prep()
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
