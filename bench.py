@@ -262,18 +262,20 @@ def run_ours(args, wl, rank, world, local):
         def e2e_prep():
             pass
 
+        pinned_out = torch.empty_like(pinned_u).pin_memory()
+
         def e2e_step():
-            # the public call a user makes: host patches in, swept patches out
-            b = sl.PatchBatch(pinned_u, pinned_f, wl.omega, device=dev)
-            b.sweep(kind, wl.sweeps, flags=flags)
-            return b.values()
+            # the public calls a user makes: host patches in, swept patches out
+            pb.upload(pinned_u, pinned_f)
+            pb.sweep(kind, wl.sweeps, flags=flags)
+            return pb.values(out=pinned_out)
     else:
         mesh = sl.Mesh(wl.dim, wl.n, device=dev)
         sl.init(mesh, wl.seed)
         sl.init_rhs(mesh, wl.seed + 1, wl.omega)
         plan = sl.SweepPlan(mesh, kind, cost)
         u0_host = mesh.values.copy()
-        f_host = mesh._rhs_host
+        f_host = torch.from_numpy(mesh._rhs_host).pin_memory()
 
         def step():
             sl.run_sweeps(mesh, kind, cost, wl.sweeps, plan=plan, flags=flags)

@@ -138,11 +138,17 @@ class Mesh:
             self.omega = None
             return
         torch = _torch()
-        if isinstance(f, torch.Tensor):
+        if isinstance(f, torch.Tensor) and f.is_cuda:
             if f.numel() != self.size or f.dtype != torch.float64:
                 raise ValueError("rhs must be float64 with (n+2)^dim elements")
             self._rhs_host = None
             self._rhs_dev = f.reshape(-1)
+        elif isinstance(f, torch.Tensor):
+            # host tensor (pinned ones upload asynchronously)
+            if f.numel() != self.size or f.dtype != torch.float64:
+                raise ValueError("rhs must be float64 with (n+2)^dim elements")
+            self._rhs_host = f.reshape(-1)
+            self._rhs_dev = None
         else:
             f = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
             if f.size != self.size:
@@ -158,7 +164,10 @@ class Mesh:
     def rhs_device(self):
         if self._rhs_dev is None and self._rhs_host is not None:
             torch = _torch()
-            self._rhs_dev = torch.from_numpy(self._rhs_host).to(self._torch_device())
+            host = self._rhs_host
+            if not isinstance(host, torch.Tensor):
+                host = torch.from_numpy(host)
+            self._rhs_dev = host.to(self._torch_device(), non_blocking=True)
         return self._rhs_dev
 
     def workspace(self, nbytes: int):

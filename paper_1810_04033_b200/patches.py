@@ -44,8 +44,23 @@ class PatchBatch:
         self.n = u.shape[1] - 2
         self.status = torch.zeros(1, dtype=torch.int32, device=dev)
 
-    def values(self) -> np.ndarray:
-        return self.u.cpu().numpy()
+    def upload(self, u, f=None):
+        """Copy new patch values (and rhs) from the host into the device buffers
+        (pinned CPU tensors copy asynchronously on the current stream)."""
+        import torch
+        self.u.copy_(torch.as_tensor(u, dtype=torch.float64).reshape(self.u.shape), non_blocking=True)
+        if f is not None:
+            if self.f is None:
+                raise ValueError("this batch was built without a right-hand side")
+            self.f.copy_(torch.as_tensor(f, dtype=torch.float64).reshape(self.f.shape), non_blocking=True)
+
+    def values(self, out=None) -> np.ndarray:
+        """Host copy of the patches; `out` (a pinned CPU tensor of u's shape)
+        receives it without allocating."""
+        if out is None:
+            return self.u.cpu().numpy()
+        out.copy_(self.u)
+        return out.numpy()
 
     def _descriptors(self, kind: StencilKind):
         if kind.dim != 2:
