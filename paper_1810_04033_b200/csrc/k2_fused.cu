@@ -61,7 +61,11 @@ __device__ __forceinline__ void stg2(double *p, double a, double b) {
 
 template <int S, int M>
 struct Geo3 {
-  static constexpr FPlan P = make_plan(S, natural_colours(S), M);
+  // lags spread so that all phases of a step are independent (plan.cuh):
+  // one block barrier per step.  FE27 (26 neighbours) would need a window of
+  // 8 lags, so it keeps per-phase barriers.
+  static constexpr bool SPREAD = (S != FE27);
+  static constexpr FPlan P = make_plan(S, natural_colours(S), M, SPREAD);
   static constexpr int K = P.K, C = P.C, LAGMAX = P.lagmax;
   static constexpr bool RB = (P.C == 2);
   static constexpr int GX = even_up(P.load[0]);
@@ -73,14 +77,14 @@ struct Geo3 {
   static constexpr int PY = 32;
   static constexpr int TX = PX - 2 * GX;
   static constexpr int TY = PY - 2 * GY;
-  static constexpr int W = 4;                // u plane slots (>= LAGMAX + 3, power of 2)
-  static constexpr int WF = 2;               // f plane slots (>= LAGMAX + 1, power of 2)
+  static constexpr int W = LAGMAX + 3;       // u plane slots: t-LAGMAX-1 .. t+1
+  static constexpr int WF = LAGMAX + 1;      // f plane slots: t-LAGMAX .. t
   static constexpr int SLOT = PY * ROWW;
   static constexpr int RSTEP = RB ? 1 : 2;   // point rows of one colour
   static constexpr int RY = RB ? 4 : (S == Q1 || S == FE27 ? 1 : 2);  // point rows per warp item
-  static constexpr int MINB = (S == FE27) ? 1 : 2;  // CTAs/SM (register budget)
+  static constexpr int NT = (S == Q1 || S == FE27) ? 256 : 512;  // Q1/FE27: 255-register budget
+  static constexpr int MINB = 1;
   static constexpr int PAD_ROWS = (RY - 1) * RSTEP + 2;
-  static constexpr int NT = 256;
   static constexpr int NW = NT / 32;
   static constexpr int PAIRS = PY * PX / 2;
   static constexpr int LPT = PAIRS / NT;
@@ -88,7 +92,7 @@ struct Geo3 {
   static constexpr size_t SMEM = size_t((W + WF) * SLOT + PAD_ROWS * ROWW) * sizeof(double);
   static_assert(PAIRS % NT == 0, "plane load split");
   static_assert(TX >= 8 && TY >= 4, "ghost margin too wide for the tile");
-  static_assert(W >= LAGMAX + 3 && WF >= LAGMAX + 1, "window too short for the lag");
+  static_assert(SMEM <= 227 * 1024, "window exceeds shared memory");
 };
 
 template <int S, int M>
@@ -187,7 +191,7 @@ __host__ __device__ constexpr int x_parity(int colours, int c, int qy, int qz) {
 // 3D: z-streaming over (TX x TY) tiles
 
 template <int S, int FORM, bool UNIT, int DIV, int M>
-__global__ void __launch_bounds__(256, Geo3<S, M>::MINB)
+__global__ void __launch_bounds__(Geo3<S, M>::NT, Geo3<S, M>::MINB)
 k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, Tiles tl) {
   using G = Geo3<S, M>;
   constexpr FPlan P = G::P;
@@ -240,8 +244,9 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
       sm[off + soff[k] + G::HW] = r[k].y;
     }
   };
-  auto uslot = [](int gz) -> int { return (gz & (G::W - 1)) * G::SLOT; };
-  auto fslot = [](int gz) -> int { return G::FOFF + (gz & (G::WF - 1)) * G::SLOT; };
+  // planes touched are >= z0 - GZ - 1 >= -GZ - 1
+  auto uslot = [](int gz) -> int { return ((gz + 64 * G::W) % G::W) * G::SLOT; };
+  auto fslot = [](int gz) -> int { return G::FOFF + ((gz + 64 * G::WF) % G::WF) * G::SLOT; };
 
   const int t_begin = z0 - G::GZ - 1;
   const int t_end = z1 - 1 + G::LAGMAX;
@@ -259,7 +264,9 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
     if (t + 2 < zlim) load_regs(src, t + 2, pu);
     if (FORM == 1 && t + 1 < zlim) load_regs(p.f, t + 1, pf);
 
-    // ---- colour phases, in order ----
+    // ---- colour phases, in order; with spread lags they are independent and
+    // their warp items are pooled (phase J starts where J-1's items ended) ----
+    int ibase = 0;
     [&]<int... Js>(std::integer_sequence<int, Js...>) {
       (
           [&] {
@@ -283,7 +290,9 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
             const bool ok0 = xok(S0, nx_), ok1 = xok(S0 ^ 1, nx_);
             const int um = uslot(pz - 1) + lane, uc = uslot(pz) + lane, up = uslot(pz + 1) + lane;
             const int fo0 = fslot(pz) + lane;
-            for (int it = warp; it < nitems; it += G::NW) {
+            int first = G::SPREAD ? (warp - ibase) % G::NW : warp;
+            if (first < 0) first += G::NW;
+            for (int it = first; it < nitems; it += G::NW) {
               const int ly0 = ly_lo + it * G::RY * G::RSTEP;
               unsigned vmask = 0;
 #pragma unroll
@@ -297,10 +306,15 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
               auto fo = [&](int r) -> int { return fo0 + (ly0 + r * G::RSTEP) * G::ROWW; };
               bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, S0>(ro, fo, vmask, p);
             }
-            __syncthreads();
+            ibase += nitems;
+            if (!G::SPREAD)
+              __syncthreads();
+            else
+              asm volatile("" ::: "memory");  // keep phases' register live ranges apart
           }(),
           ...);
     }(std::make_integer_sequence<int, G::K>{});
+    if (G::SPREAD) __syncthreads();
 
     // ---- finished plane of the owned box -> dst ----
     const int gz_out = t - G::LAGMAX;
