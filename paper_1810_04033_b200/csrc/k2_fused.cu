@@ -78,49 +78,19 @@ struct Geo3 {
   static constexpr int TX = PX - 2 * GX;
   static constexpr int TY = PY - 2 * GY;
   static constexpr int W = LAGMAX + 3;       // u plane slots: t-LAGMAX-1 .. t+1
-  static constexpr int WF = LAGMAX + 1;      // f plane slots: t-LAGMAX .. t
   static constexpr int SLOT = PY * ROWW;
   static constexpr int RSTEP = RB ? 1 : 2;   // point rows of one colour
   static constexpr int RY = RB ? 4 : (S == Q1 || S == FE27 ? 1 : 2);  // point rows per warp item
-  static constexpr int NT = (S == Q1 || S == FE27) ? 256 : 512;  // Q1/FE27: 255-register budget
-  static constexpr int MINB = 1;
+  static constexpr int NT = 256;
+  static constexpr int MINB = (S == Q1 || S == FE27) ? 1 : 2;  // Q1/FE27: 255-register budget
   static constexpr int PAD_ROWS = (RY - 1) * RSTEP + 2;
   static constexpr int NW = NT / 32;
   static constexpr int PAIRS = PY * PX / 2;
   static constexpr int LPT = PAIRS / NT;
-  static constexpr int FOFF = W * SLOT;
-  static constexpr size_t SMEM = size_t((W + WF) * SLOT + PAD_ROWS * ROWW) * sizeof(double);
+  static constexpr size_t SMEM = size_t(W * SLOT + PAD_ROWS * ROWW) * sizeof(double);
   static_assert(PAIRS % NT == 0, "plane load split");
   static_assert(TX >= 8 && TY >= 4, "ghost margin too wide for the tile");
   static_assert(SMEM <= 227 * 1024, "window exceeds shared memory");
-};
-
-template <int S, int M>
-struct Geo2 {
-  static constexpr FPlan P = make_plan(S, natural_colours(S), M);
-  static constexpr int K = P.K, C = P.C, LAGMAX = P.lagmax;
-  static constexpr bool RB = (P.C == 2);
-  static constexpr int GX = even_up(P.load[0]);
-  static constexpr int GY = P.load[1];       // streaming-axis margin
-  static constexpr int NSTRIP = 4;
-  static constexpr int PX = 64 * NSTRIP;
-  static constexpr int HW = PX / 2 + 2;
-  static constexpr int ROWW = 2 * HW;
-  static constexpr int R = 8;                // rows per macro-step
-  static constexpr int WR = 32;              // u rows resident (4 blocks, power of 2)
-  static constexpr int WRF = 16;             // f rows resident (2 blocks)
-  static constexpr int TX = PX - 2 * GX;
-  static constexpr int RSTEP = RB ? 1 : 2;
-  static constexpr int RY = RB ? 4 : 2;
-  static constexpr int NT = 256;
-  static constexpr int NW = NT / 32;
-  static constexpr int PAIRS = R * PX / 2;
-  static constexpr int LPT = PAIRS / NT;
-  static constexpr int FOFF = WR * ROWW;
-  static constexpr size_t SMEM = size_t((WR + WRF) * ROWW) * sizeof(double);
-  static_assert(LAGMAX + 1 <= R, "row block shorter than the phase lag");
-  static_assert(PAIRS % NT == 0, "block load split");
-  static_assert(WR >= 3 * R && WRF >= 2 * R, "window too short");
 };
 
 struct Tiles {
@@ -143,12 +113,12 @@ __device__ __forceinline__ unsigned nonfinite_bits(double v) {
 // one warp item: RY point rows of a 32-lane strip, x parity pattern fixed at
 // compile time (S0 = parity of row 0; red-black rows alternate).
 //   ro(dz, k): smem element offset of source row k of plane dz (point row r
-//   uses k = r*RSTEP + dy + 1), lane included;  fo(r): f offset of point row r.
+//   uses k = r*RSTEP + dy + 1), lane included;  fv(r, s): f of point row r.
 // All loads precede all stores, so repeated (row, x) loads are CSE'd.
 
 template <int S, int FORM, bool UNIT, int DIV, int RY, int RSTEP, bool RB, int HW, int S0,
           typename RowOff, typename FOff>
-__device__ __forceinline__ unsigned update_item(const RowOff &ro, const FOff &fo, unsigned vmask,
+__device__ __forceinline__ unsigned update_item(const RowOff &ro, const FOff &fv, unsigned vmask,
                                                 const Params &p) {
   extern __shared__ double sm[];
   constexpr int NNZ = shape_nnz(S);
@@ -165,7 +135,7 @@ __device__ __forceinline__ unsigned update_item(const RowOff &ro, const FOff &fo
       acc = acc_add<FORM, UNIT>(acc, sm[ro(o.z + 1, kc + o.y) + xoff<HW>(s, o.x)], q, p);
     }
     double fc = 0.0;
-    if (FORM == 1) fc = sm[fo(r) + xoff<HW>(s, 0)];
+    if (FORM == 1) fc = fv(r, s);
     out[r] = acc_finish<FORM, UNIT, DIV>(acc, uc, fc, p);
   }
   unsigned bad = 0;
@@ -244,25 +214,21 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
       sm[off + soff[k] + G::HW] = r[k].y;
     }
   };
-  // planes touched are >= z0 - GZ - 1 >= -GZ - 1
-  auto uslot = [](int gz) -> int { return ((gz + 64 * G::W) % G::W) * G::SLOT; };
-  auto fslot = [](int gz) -> int { return G::FOFF + ((gz + 64 * G::WF) % G::WF) * G::SLOT; };
-
   const int t_begin = z0 - G::GZ - 1;
   const int t_end = z1 - 1 + G::LAGMAX;
   const int zlim = z1 + G::GZ;
-  double2 pu[G::LPT], pf[G::LPT];
+  int so[G::W];  // so[k] = smem offset of the slot holding plane t+1-k (rotated per step)
+#pragma unroll
+  for (int k = 0; k < G::W; ++k) so[k] = (((t_begin + 1 - k) % G::W + G::W) % G::W) * G::SLOT;
+  double2 pu[G::LPT];
   load_regs(src, t_begin + 1, pu);
-  if (FORM == 1) load_regs(p.f, t_begin, pf);
 
   unsigned bad = 0;
   for (int t = t_begin; t <= t_end; ++t) {
-    // planes loaded during the previous step go into their (free) slots
-    if (t + 1 < zlim) store_regs(uslot(t + 1), pu);
-    if (FORM == 1 && t < zlim) store_regs(fslot(t), pf);
+    // the plane loaded during the previous step goes into its (free) slot
+    if (t + 1 < zlim) store_regs(so[0], pu);
     __syncthreads();
     if (t + 2 < zlim) load_regs(src, t + 2, pu);
-    if (FORM == 1 && t + 1 < zlim) load_regs(p.f, t + 1, pf);
 
     // ---- colour phases, in order; with spread lags they are independent and
     // their warp items are pooled (phase J starts where J-1's items ended) ----
@@ -288,8 +254,8 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
             const int npr = ly_hi > ly_lo ? (ly_hi - ly_lo + G::RSTEP - 1) / G::RSTEP : 0;
             const int nitems = (npr + G::RY - 1) / G::RY;
             const bool ok0 = xok(S0, nx_), ok1 = xok(S0 ^ 1, nx_);
-            const int um = uslot(pz - 1) + lane, uc = uslot(pz) + lane, up = uslot(pz + 1) + lane;
-            const int fo0 = fslot(pz) + lane;
+            const int um = so[P.lag[J] + 2] + lane, uc = so[P.lag[J] + 1] + lane, up = so[P.lag[J]] + lane;
+            const double *fpl = FORM == 1 ? p.f + (int64_t)pz * p.sz : nullptr;
             int first = G::SPREAD ? (warp - ibase) % G::NW : warp;
             if (first < 0) first += G::NW;
             for (int it = first; it < nitems; it += G::NW) {
@@ -303,8 +269,11 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
               }
               const int rb = (ly0 - 1) * G::ROWW;
               auto ro = [&](int d, int k) -> int { return (d == 0 ? um : (d == 1 ? uc : up)) + rb + k * G::ROWW; };
-              auto fo = [&](int r) -> int { return fo0 + (ly0 + r * G::RSTEP) * G::ROWW; };
-              bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, S0>(ro, fo, vmask, p);
+              const double *frow0 = fpl + (int64_t)(gy0 + ly0) * p.sy + gx0 + 2 * lane;
+              auto fv = [&](int r, int s) -> double {
+                return ((vmask >> r) & 1) ? __ldg(frow0 + (int64_t)r * G::RSTEP * p.sy + s) : 0.0;
+              };
+              bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, S0>(ro, fv, vmask, p);
             }
             ibase += nitems;
             if (!G::SPREAD)
@@ -319,141 +288,17 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
     // ---- finished plane of the owned box -> dst ----
     const int gz_out = t - G::LAGMAX;
     if (gz_out >= z0 && gz_out < z1) {
-      const int so = uslot(gz_out);
+      const int sout = so[G::LAGMAX + 1];
       double *pb = dst + (int64_t)gz_out * p.sz;
 #pragma unroll
       for (int k = 0; k < G::LPT; ++k)
-        if ((ownm >> k) & 1) stg2(pb + goff[k], sm[so + soff[k]], sm[so + soff[k] + G::HW]);
+        if ((ownm >> k) & 1) stg2(pb + goff[k], sm[sout + soff[k]], sm[sout + soff[k] + G::HW]);
     }
-  }
-  if (bad) atomicOr(p.status, 1);
-}
-
-// ---------------------------------------------------------------------------
-// 2D: y-streaming in row blocks of R over TX-column tiles
-
-template <int S, int FORM, bool UNIT, int DIV, int M>
-__global__ void __launch_bounds__(256, 2)
-k2_stream2d(Params p, const double *__restrict__ src, double *__restrict__ dst, Tiles tl) {
-  using G = Geo2<S, M>;
-  constexpr FPlan P = G::P;
-  extern __shared__ double sm[];
-
-  const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2;
-  const int nx = (int)p.nx, ny = (int)p.ny;
-  const int item = blockIdx.x;
-  const int tx = item % (int)tl.ntx;
-  const int yc = item / (int)tl.ntx;
-  const int x0 = (int)tile_start(tx, Sx, tl.ntx), x1 = (int)tile_start(tx + 1, Sx, tl.ntx);
-  const int y0 = (int)chunk_start(yc, Sy, tl.nty), y1 = (int)chunk_start(yc + 1, Sy, tl.nty);
-  const int TXo = x1 - x0;
-  const int gx0 = x0 - G::GX;
-  const int yb = y0 - G::GY;  // first row of block 0; rows touched are >= yb - 1
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  auto urow = [&](int gy) -> int { return ((gy - yb + G::WR) & (G::WR - 1)) * G::ROWW; };
-  auto frow = [&](int gy) -> int { return G::FOFF + ((gy - yb) & (G::WRF - 1)) * G::ROWW; };
-
-  auto load_regs = [&](const double *base, int blk, int ylim, double2 (&r)[G::LPT]) {
+    {  // rotate: the slot of plane t-LAGMAX-1 becomes the slot of plane t+2
+      const int tmp = so[G::W - 1];
 #pragma unroll
-    for (int k = 0; k < G::LPT; ++k) {
-      const int pair = tid + k * G::NT;
-      const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      const int gx = gx0 + 2 * i, gy = yb + blk * G::R + row;
-      const bool ok = gy >= 0 && gy < Sy && gy < ylim && gx >= 0 && gx < Sx;
-      r[k] = ok ? ldg_nc2(base + (int64_t)gy * p.sy + gx) : make_double2(0.0, 0.0);
-    }
-  };
-  auto store_regs = [&](bool is_f, int blk, const double2 (&r)[G::LPT]) {
-#pragma unroll
-    for (int k = 0; k < G::LPT; ++k) {
-      const int pair = tid + k * G::NT;
-      const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      const int gy = yb + blk * G::R + row;
-      const int off = is_f ? frow(gy) : urow(gy);
-      sm[off + 1 + i] = r[k].x;
-      sm[off + G::HW + 1 + i] = r[k].y;
-    }
-  };
-
-  const int ylim = y1 + G::GY;
-  const int T_end = (y1 - 1 + G::LAGMAX - yb) / G::R;
-  double2 pu[G::LPT], pf[G::LPT];
-  load_regs(src, 0, ylim, pu);
-  store_regs(false, 0, pu);
-  load_regs(src, 1, ylim, pu);
-  if (FORM == 1) load_regs(p.f, 0, ylim, pf);
-
-  unsigned bad = 0;
-  for (int T = 0; T <= T_end; ++T) {
-    store_regs(false, T + 1, pu);
-    if (FORM == 1) store_regs(true, T, pf);
-    __syncthreads();
-    if (yb + (T + 2) * G::R < ylim) load_regs(src, T + 2, ylim, pu);
-    if (FORM == 1 && yb + (T + 1) * G::R < ylim) load_regs(p.f, T + 1, ylim, pf);
-    const int front = yb + T * G::R;
-
-    [&]<int... Js>(std::integer_sequence<int, Js...>) {
-      (
-          [&] {
-            constexpr int J = Js;
-            constexpr int c = P.colour[J];
-            constexpr int nx_ = P.need[J][0], ny_ = P.need[J][1];
-            int r_lo = front - P.lag[J], r_hi = r_lo + G::R;  // [lo, hi)
-            if (r_lo < 1) r_lo = 1;
-            if (r_lo < y0 - ny_) r_lo = y0 - ny_;
-            if (r_hi > ny + 1) r_hi = ny + 1;
-            if (r_hi > y1 + ny_) r_hi = y1 + ny_;
-            if (r_lo >= r_hi) return;
-            const int r_first = r_lo;
-            const int want_qy = G::RB ? ((1 + c) & 1) : ((c >> 1) & 1);
-            if (((r_lo - 1 + p.py) & 1) != want_qy) --r_lo;
-            constexpr int S0 = G::RB ? 0 : x_parity(G::C, c, (c >> 1) & 1, 0);
-            const int npr = (r_hi - r_lo + G::RSTEP - 1) / G::RSTEP;
-            const int ngrp = (npr + G::RY - 1) / G::RY;
-            const int lx_lo = G::GX - nx_, lx_hi = G::GX + TXo + nx_;
-            for (int it = warp; it < ngrp * G::NSTRIP; it += G::NW) {
-              const int strip = it & (G::NSTRIP - 1);
-              const int row0 = r_lo + (it / G::NSTRIP) * G::RY * G::RSTEP;
-              const int li = strip * 32 + lane;
-              const int gxl = gx0 + 2 * li;
-              unsigned vmask = 0;
-#pragma unroll
-              for (int r = 0; r < G::RY; ++r) {
-                const int s = G::RB ? (S0 ^ ((r * G::RSTEP) & 1)) : S0;
-                const int lx = 2 * li + s;
-                const int row = row0 + r * G::RSTEP;
-                const bool v = row >= r_first && row < r_hi && lx >= lx_lo && lx < lx_hi &&
-                               gxl + s >= 1 && gxl + s <= nx;
-                vmask |= (unsigned)v << r;
-              }
-              constexpr int NR = (G::RY - 1) * G::RSTEP + 3;
-              int rw[NR];
-#pragma unroll
-              for (int k = 0; k < NR; ++k) rw[k] = urow(row0 - 1 + k) + li;
-              int fw[G::RY];
-#pragma unroll
-              for (int r = 0; r < G::RY; ++r) fw[r] = frow(row0 + r * G::RSTEP) + li;
-              auto ro = [&](int, int k) -> int { return rw[k]; };
-              auto fo = [&](int r) -> int { return fw[r]; };
-              bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, S0>(ro, fo, vmask, p);
-            }
-            __syncthreads();
-          }(),
-          ...);
-    }(std::make_integer_sequence<int, G::K>{});
-
-    // finished rows [front - LAGMAX, front + R - LAGMAX) of the owned box -> dst
-#pragma unroll
-    for (int k = 0; k < G::LPT; ++k) {
-      const int pair = tid + k * G::NT;
-      const int row = pair / (G::PX / 2), i = pair % (G::PX / 2);
-      const int gy = front - G::LAGMAX + row;
-      const int lx = 2 * i;
-      if (gy >= y0 && gy < y1 && lx >= G::GX && lx < G::GX + TXo) {
-        const int ro = urow(gy);
-        stg2(dst + (int64_t)gy * p.sy + gx0 + lx, sm[ro + 1 + i], sm[ro + G::HW + 1 + i]);
-      }
+      for (int k = G::W - 1; k > 0; --k) so[k] = so[k - 1];
+      so[0] = tmp;
     }
   }
   if (bad) atomicOr(p.status, 1);
