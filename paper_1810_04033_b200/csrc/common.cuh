@@ -118,6 +118,31 @@ __device__ __forceinline__ double acc_finish(double acc, double uc, double fc, c
   return __dadd_rn(uc, __dmul_rn(p.omega, q));
 }
 
+// Hot-loop division: the exact fallback runs only for lanes whose result is
+// used (`used`); ghost/padding lanes may hold zeros or garbage.  The range
+// test is on the exponent field: fast path iff 2^-959 <= |a| < 2^960.
+template <int DIV>
+__device__ __forceinline__ double div_wc_used(double a, bool used, const Params &p) {
+  if (DIV == DIV_POW2) return __dmul_rn(a, p.rwc);
+  if (DIV == DIV_RCP) {
+    const unsigned e = ((unsigned)__double2hiint(a) >> 20) & 0x7ffu;
+    const double q0 = __dmul_rn(a, p.rwc);
+    const double r = __fma_rn(-p.wc, q0, a);
+    double q = __fma_rn(r, p.rwc, q0);
+    if (__builtin_expect(used && (e - 64u) >= 1919u, 0)) q = __ddiv_rn(a, p.wc);
+    return q;
+  }
+  return __ddiv_rn(a, p.wc);
+}
+
+template <int FORM, bool UNIT, int DIV>
+__device__ __forceinline__ double acc_finish_used(double acc, double uc, double fc, bool used,
+                                                  const Params &p) {
+  if (FORM == 0) return div_wc_used<DIV>(acc, used, p);
+  const double q = div_wc_used<DIV>(__dsub_rn(fc, acc), used, p);
+  return __dadd_rn(uc, __dmul_rn(p.omega, q));
+}
+
 __device__ __forceinline__ bool finite64(double v) {
   // exponent bits not all ones
   return (__double_as_longlong(v) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;

@@ -136,7 +136,7 @@ __device__ __forceinline__ unsigned update_item(const RowOff &ro, const FOff &fv
     }
     double fc = 0.0;
     if (FORM == 1) fc = fv(r, s);
-    out[r] = acc_finish<FORM, UNIT, DIV>(acc, uc, fc, p);
+    out[r] = acc_finish_used<FORM, UNIT, DIV>(acc, uc, fc, (vmask >> r) & 1, p);
   }
   unsigned bad = 0;
 #pragma unroll
@@ -255,7 +255,8 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
             const int nitems = (npr + G::RY - 1) / G::RY;
             const bool ok0 = xok(S0, nx_), ok1 = xok(S0 ^ 1, nx_);
             const int um = so[P.lag[J] + 2] + lane, uc = so[P.lag[J] + 1] + lane, up = so[P.lag[J]] + lane;
-            const double *fpl = FORM == 1 ? p.f + (int64_t)pz * p.sz : nullptr;
+            const int sy = (int)p.sy;
+            const double *fpl = FORM == 1 ? p.f + (int64_t)pz * p.sz + gy0 * sy + gx0 + 2 * lane : nullptr;
             int first = G::SPREAD ? (warp - ibase) % G::NW : warp;
             if (first < 0) first += G::NW;
             for (int it = first; it < nitems; it += G::NW) {
@@ -269,9 +270,9 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
               }
               const int rb = (ly0 - 1) * G::ROWW;
               auto ro = [&](int d, int k) -> int { return (d == 0 ? um : (d == 1 ? uc : up)) + rb + k * G::ROWW; };
-              const double *frow0 = fpl + (int64_t)(gy0 + ly0) * p.sy + gx0 + 2 * lane;
+              const double *frow0 = fpl + ly0 * sy;
               auto fv = [&](int r, int s) -> double {
-                return ((vmask >> r) & 1) ? __ldg(frow0 + (int64_t)r * G::RSTEP * p.sy + s) : 0.0;
+                return ((vmask >> r) & 1) ? __ldg(frow0 + r * G::RSTEP * sy + s) : 0.0;
               };
               bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, S0>(ro, fv, vmask, p);
             }

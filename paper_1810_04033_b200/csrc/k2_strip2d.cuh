@@ -86,22 +86,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
       : "memory");
 }
 
-// Markstein-corrected division for the hot loop: the fallback runs only for
-// lanes whose result is used (ghost lanes may hold zeros or garbage).
-template <int DIV>
-__device__ __forceinline__ double div_wc_lane(double a, bool used, const Params &p) {
-  if (DIV == DIV_POW2) return __dmul_rn(a, p.rwc);
-  if (DIV == DIV_RCP) {
-    const unsigned e = ((unsigned)__double2hiint(a) >> 20) & 0x7ffu;
-    const double q0 = __dmul_rn(a, p.rwc);
-    const double r = __fma_rn(-p.wc, q0, a);
-    double q = __fma_rn(r, p.rwc, q0);
-    if (__builtin_expect(used && (e - 64u) >= 1918u, 0)) q = __ddiv_rn(a, p.wc);  // |a| outside [2^-959, 2^959)
-    return q;
-  }
-  return __ddiv_rn(a, p.wc);
-}
-
 template <int S, int FORM, bool UNIT, int DIV, int M>
 __global__ void __launch_bounds__(32 * GeoS2<S, M>::WPB)
 k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, int64_t nstrip,
@@ -253,9 +237,9 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                           acc = acc_add<FORM, UNIT>(acc, val(o.y + 1, o.x), q, p);
                         }
                         if (FORM == 0) {
-                          outv[k] = div_wc_lane<DIV>(acc, valid[k], p);
+                          outv[k] = div_wc_used<DIV>(acc, valid[k], p);
                         } else {
-                          const double qd = div_wc_lane<DIV>(__dsub_rn(ff[R0][cc], acc), valid[k], p);
+                          const double qd = div_wc_used<DIV>(__dsub_rn(ff[R0][cc], acc), valid[k], p);
                           outv[k] = __dadd_rn(uc, __dmul_rn(p.omega, qd));
                         }
                       }
