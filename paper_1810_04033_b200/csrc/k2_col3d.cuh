@@ -2,8 +2,8 @@
 // column-owning 2.5D streaming with TMA plane loads.
 //
 // A CTA owns a 64 x 32 tile of (x, y) columns (plus the ghost margin of the
-// plan) and a chunk of z.  Thread (warp w, lane i) owns row w, column pair
-// (2i, 2i+1) of the tile for the whole chunk.  For the face stencil every
+// plan) and a chunk of z.  Thread (warp w, lane i) owns rows w and w+16 and
+// column pair (2i, 2i+1) of the tile for the whole chunk.  For the face stencil every
 // z-neighbour of a point lies in the same column, so each thread keeps its
 // column's values for planes t-3 .. t+1 in a register ring; only in-plane
 // (x+-1, y+-1) neighbours are read from shared memory.
@@ -34,7 +34,8 @@ struct Col3Geo {
   static constexpr int TX = PX - 2 * GX, TY = PY - 2 * GY;
   static constexpr int R = 6;                              // ring length (registers, smem slots)
   static constexpr int D = 2;                              // TMA lookahead beyond plane t+1
-  static constexpr int NT = 32 * PY;                       // one warp per tile row
+  static constexpr int RT = 2;                             // tile rows per thread (w, w + PY/RT)
+  static constexpr int NT = 32 * PY / RT;
   static constexpr int SLOTE = PX * PY;                    // doubles per plane slot
   static constexpr int PADE = 16;                          // guard elements before/after the ring
   static constexpr size_t SMEM = size_t(2 * R * SLOTE + 2 * PADE) * sizeof(double) + 2 * R * 8;
@@ -92,9 +93,8 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
   const int z0 = (int)(((int64_t)zc * Sz) / nzc), z1 = (int)(((int64_t)(zc + 1) * Sz) / nzc);
   const int TXo = x1 - x0, TYo = y1 - y0;
   const int gx0 = x0 - G::GX, gy0 = y0 - G::GY;
-  const int lane = threadIdx.x & 31, ly = threadIdx.x >> 5;
-  const int gy = gy0 + ly, gx = gx0 + 2 * lane;
-  const int qy = (gy - 1 + p.py) & 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gx = gx0 + 2 * lane;
 
   // ring slot k holds plane t_begin + k (mod R); plane parity of slot k is k & 1
   int t_begin = z0 - G::GZ - 1;
@@ -126,19 +126,30 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
 
   // phase row/col windows (tile-local); red = phase 0 (need 1), black = phase 1 (need 0)
   const int n0x = G::P.need[0][0], n0y = G::P.need[0][1], n0z = G::P.need[0][2];
-  const bool row0 = ly >= G::GY - n0y && ly < G::GY + TYo + n0y && gy >= 1 && gy <= ny;
-  const bool row1 = ly >= G::GY && ly < G::GY + TYo && gy >= 1 && gy <= ny;
   auto colok = [&](int s, int need) -> bool {
     const int lx = 2 * lane + s;
     return lx >= G::GX - need && lx < G::GX + TXo + need && gx + s >= 1 && gx + s <= nx;
   };
-  const bool own_out = ly >= G::GY && ly < G::GY + TYo && 2 * lane >= G::GX && 2 * lane < G::GX + TXo;
-
-  double U[R][2];
+  const bool xown = 2 * lane >= G::GX && 2 * lane < G::GX + TXo;
+  int ly[G::RT], gy[G::RT], qy[G::RT], rowoff[G::RT];
+  bool row0[G::RT], row1[G::RT], own_out[G::RT];
 #pragma unroll
-  for (int k = 0; k < R; ++k) U[k][0] = U[k][1] = 0.0;
+  for (int r = 0; r < G::RT; ++r) {
+    ly[r] = warp + r * (G::PY / G::RT);
+    gy[r] = gy0 + ly[r];
+    qy[r] = (gy[r] - 1 + p.py) & 1;
+    rowoff[r] = ly[r] * G::PX + 2 * lane;  // element offset of the thread's pair in a slot
+    row0[r] = ly[r] >= G::GY - n0y && ly[r] < G::GY + TYo + n0y && gy[r] >= 1 && gy[r] <= ny;
+    row1[r] = ly[r] >= G::GY && ly[r] < G::GY + TYo && gy[r] >= 1 && gy[r] <= ny;
+    own_out[r] = ly[r] >= G::GY && ly[r] < G::GY + TYo && xown;
+  }
 
-  const int rowoff = ly * G::PX + 2 * lane;  // element offset of the thread's pair in a slot
+  double U[G::RT][R][2];
+#pragma unroll
+  for (int r = 0; r < G::RT; ++r)
+#pragma unroll
+    for (int k = 0; k < R; ++k) U[r][k][0] = U[r][k][1] = 0.0;
+
   unsigned bad = 0;
   uint32_t round = 0;
   for (int t0 = t_begin; t0 <= t_end; t0 += R, ++round) {
@@ -153,9 +164,12 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
             {
               const uint32_t use = round + (uint32_t)((KS + 1) / R);
               mbar_wait3(mb_s + 8u * S1, (use - (S1 == 0 ? 1u : 0u)) & 1u);
-              const double2 v = *reinterpret_cast<const double2 *>(su + S1 * G::SLOTE + rowoff);
-              U[S1][0] = v.x;
-              U[S1][1] = v.y;
+#pragma unroll
+              for (int r = 0; r < G::RT; ++r) {
+                const double2 v = *reinterpret_cast<const double2 *>(su + S1 * G::SLOTE + rowoff[r]);
+                U[r][S1][0] = v.x;
+                U[r][S1][1] = v.y;
+              }
             }
             if (FORM == 1) {
               const uint32_t use = round + (uint32_t)(KS / R);
@@ -164,54 +178,64 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
             constexpr int qz = KS & 1;  // (t - 1 + pz) & 1
             // ---- red (colour 0) at plane t ----
             if (t >= 1 && t <= nz && t >= z0 - n0z && t < z1 + n0z) {
-              const int s = 1 ^ ((qy + qz) & 1);  // x parity of the red point in the pair
-              const double *pl = su + S0 * G::SLOTE + rowoff + s;
-              const double uc = s ? U[S0][1] : U[S0][0];
-              const double vzm = s ? U[SM1][1] : U[SM1][0];
-              const double vzp = s ? U[S1][1] : U[S1][0];
-              double acc = acc_init<FORM, UNIT>(uc, p);
-              acc = acc_add<FORM, UNIT>(acc, vzm, 0, p);            // (0,0,-1)
-              acc = acc_add<FORM, UNIT>(acc, pl[-G::PX], 1, p);     // (0,-1,0)
-              acc = acc_add<FORM, UNIT>(acc, pl[-1], 2, p);         // (-1,0,0)
-              acc = acc_add<FORM, UNIT>(acc, pl[1], 3, p);          // (1,0,0)
-              acc = acc_add<FORM, UNIT>(acc, pl[G::PX], 4, p);      // (0,1,0)
-              acc = acc_add<FORM, UNIT>(acc, vzp, 5, p);            // (0,0,1)
-              const bool ok = row0 && colok(s, n0x);
-              const double fc = FORM == 1 ? sf[S0 * G::SLOTE + rowoff + s] : 0.0;
-              const double out = acc_finish_used<FORM, UNIT, DIV>(acc, uc, fc, ok, p);
-              if (ok) {
-                if (s) U[S0][1] = out; else U[S0][0] = out;
-                su[S0 * G::SLOTE + rowoff + s] = out;
+#pragma unroll
+              for (int r = 0; r < G::RT; ++r) {
+                const int s = 1 ^ ((qy[r] + qz) & 1);  // x parity of the red point in the pair
+                const double *pl = su + S0 * G::SLOTE + rowoff[r] + s;
+                const double uc = s ? U[r][S0][1] : U[r][S0][0];
+                const double vzm = s ? U[r][SM1][1] : U[r][SM1][0];
+                const double vzp = s ? U[r][S1][1] : U[r][S1][0];
+                double acc = acc_init<FORM, UNIT>(uc, p);
+                acc = acc_add<FORM, UNIT>(acc, vzm, 0, p);            // (0,0,-1)
+                acc = acc_add<FORM, UNIT>(acc, pl[-G::PX], 1, p);     // (0,-1,0)
+                acc = acc_add<FORM, UNIT>(acc, pl[-1], 2, p);         // (-1,0,0)
+                acc = acc_add<FORM, UNIT>(acc, pl[1], 3, p);          // (1,0,0)
+                acc = acc_add<FORM, UNIT>(acc, pl[G::PX], 4, p);      // (0,1,0)
+                acc = acc_add<FORM, UNIT>(acc, vzp, 5, p);            // (0,0,1)
+                const bool ok = row0[r] && colok(s, n0x);
+                const double fc = FORM == 1 ? sf[S0 * G::SLOTE + rowoff[r] + s] : 0.0;
+                const double out = acc_finish_used<FORM, UNIT, DIV>(acc, uc, fc, ok, p);
+                if (ok) {
+                  if (s) U[r][S0][1] = out; else U[r][S0][0] = out;
+                  su[S0 * G::SLOTE + rowoff[r] + s] = out;
+                }
               }
             }
             // ---- black (colour 1) at plane t-2 ----
             {
               const int pz = t - 2;
               if (pz >= 1 && pz <= nz && pz >= z0 && pz < z1) {
-                const int s = (qy + qz) & 1;  // the other column of the pair
-                const double *pl = su + SM2 * G::SLOTE + rowoff + s;
-                const double uc = s ? U[SM2][1] : U[SM2][0];
-                const double vzm = s ? U[SM3][1] : U[SM3][0];
-                const double vzp = s ? U[SM1][1] : U[SM1][0];
-                double acc = acc_init<FORM, UNIT>(uc, p);
-                acc = acc_add<FORM, UNIT>(acc, vzm, 0, p);
-                acc = acc_add<FORM, UNIT>(acc, pl[-G::PX], 1, p);
-                acc = acc_add<FORM, UNIT>(acc, pl[-1], 2, p);
-                acc = acc_add<FORM, UNIT>(acc, pl[1], 3, p);
-                acc = acc_add<FORM, UNIT>(acc, pl[G::PX], 4, p);
-                acc = acc_add<FORM, UNIT>(acc, vzp, 5, p);
-                const bool ok = row1 && colok(s, 0);
-                const double fc = FORM == 1 ? sf[SM2 * G::SLOTE + rowoff + s] : 0.0;
-                const double out = acc_finish_used<FORM, UNIT, DIV>(acc, uc, fc, ok, p);
-                if (ok) {
-                  if (s) U[SM2][1] = out; else U[SM2][0] = out;
+#pragma unroll
+                for (int r = 0; r < G::RT; ++r) {
+                  const int s = (qy[r] + qz) & 1;  // the other column of the pair
+                  const double *pl = su + SM2 * G::SLOTE + rowoff[r] + s;
+                  const double uc = s ? U[r][SM2][1] : U[r][SM2][0];
+                  const double vzm = s ? U[r][SM3][1] : U[r][SM3][0];
+                  const double vzp = s ? U[r][SM1][1] : U[r][SM1][0];
+                  double acc = acc_init<FORM, UNIT>(uc, p);
+                  acc = acc_add<FORM, UNIT>(acc, vzm, 0, p);
+                  acc = acc_add<FORM, UNIT>(acc, pl[-G::PX], 1, p);
+                  acc = acc_add<FORM, UNIT>(acc, pl[-1], 2, p);
+                  acc = acc_add<FORM, UNIT>(acc, pl[1], 3, p);
+                  acc = acc_add<FORM, UNIT>(acc, pl[G::PX], 4, p);
+                  acc = acc_add<FORM, UNIT>(acc, vzp, 5, p);
+                  const bool ok = row1[r] && colok(s, 0);
+                  const double fc = FORM == 1 ? sf[SM2 * G::SLOTE + rowoff[r] + s] : 0.0;
+                  const double out = acc_finish_used<FORM, UNIT, DIV>(acc, uc, fc, ok, p);
+                  if (ok) {
+                    if (s) U[r][SM2][1] = out; else U[r][SM2][0] = out;
+                  }
                 }
               }
               // ---- plane t-2 is final: owned pairs -> dst ----
-              if (pz >= z0 && pz < z1 && own_out) {
-                bad |= ((((unsigned)__double2hiint(U[SM2][0]) & 0x7ff00000u) == 0x7ff00000u) |
-                        (((unsigned)__double2hiint(U[SM2][1]) & 0x7ff00000u) == 0x7ff00000u));
-                stg_pair(dst + (int64_t)pz * p.sz + (int64_t)gy * p.sy + gx, U[SM2][0], U[SM2][1]);
+              if (pz >= z0 && pz < z1) {
+#pragma unroll
+                for (int r = 0; r < G::RT; ++r)
+                  if (own_out[r]) {
+                    bad |= ((((unsigned)__double2hiint(U[r][SM2][0]) & 0x7ff00000u) == 0x7ff00000u) |
+                            (((unsigned)__double2hiint(U[r][SM2][1]) & 0x7ff00000u) == 0x7ff00000u));
+                    stg_pair(dst + (int64_t)pz * p.sz + (int64_t)gy[r] * p.sy + gx, U[r][SM2][0], U[r][SM2][1]);
+                  }
               }
             }
             __syncthreads();
