@@ -188,8 +188,12 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
                 double acc = acc_init<FORM, UNIT>(uc, p);
                 acc = acc_add<FORM, UNIT>(acc, vzm, 0, p);            // (0,0,-1)
                 acc = acc_add<FORM, UNIT>(acc, pl[-G::PX], 1, p);     // (0,-1,0)
-                acc = acc_add<FORM, UNIT>(acc, pl[-1], 2, p);         // (-1,0,0)
-                acc = acc_add<FORM, UNIT>(acc, pl[1], 3, p);          // (1,0,0)
+                // x-neighbour inside the pair: the thread's own (black) register;
+                // across the pair boundary: the adjacent pair's value in smem
+                const double vxm = s ? U[r][S0][0] : pl[-1];
+                const double vxp = s ? pl[1] : U[r][S0][1];
+                acc = acc_add<FORM, UNIT>(acc, vxm, 2, p);            // (-1,0,0)
+                acc = acc_add<FORM, UNIT>(acc, vxp, 3, p);            // (1,0,0)
                 acc = acc_add<FORM, UNIT>(acc, pl[G::PX], 4, p);      // (0,1,0)
                 acc = acc_add<FORM, UNIT>(acc, vzp, 5, p);            // (0,0,1)
                 const bool ok = row0[r] && colok(s, n0x);
@@ -215,8 +219,10 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
                   double acc = acc_init<FORM, UNIT>(uc, p);
                   acc = acc_add<FORM, UNIT>(acc, vzm, 0, p);
                   acc = acc_add<FORM, UNIT>(acc, pl[-G::PX], 1, p);
-                  acc = acc_add<FORM, UNIT>(acc, pl[-1], 2, p);
-                  acc = acc_add<FORM, UNIT>(acc, pl[1], 3, p);
+                  const double vxm = s ? U[r][SM2][0] : pl[-1];  // own red register inside the pair
+                  const double vxp = s ? pl[1] : U[r][SM2][1];
+                  acc = acc_add<FORM, UNIT>(acc, vxm, 2, p);
+                  acc = acc_add<FORM, UNIT>(acc, vxp, 3, p);
                   acc = acc_add<FORM, UNIT>(acc, pl[G::PX], 4, p);
                   acc = acc_add<FORM, UNIT>(acc, vzp, 5, p);
                   const bool ok = row1[r] && colok(s, 0);
