@@ -112,6 +112,12 @@ SL_API int sl_colour_pass(const sl_grid *g, const sl_stencil *s, int32_t colour,
 SL_API int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats,
                     int64_t count, int32_t *d_status, void *stream);
 
+/* Ghost depth along the slowest axis (z in 3D, y in 2D) needed to run
+ * `sweeps` colour-ordered sweeps on a slab without exchanging: the input must
+ * be valid this many planes beyond the slab for its own planes to come out
+ * exact (the dependency DP of the fused schedule).  < 0 on bad arguments. */
+SL_API int sl_ghost_depth(const sl_stencil *s, int32_t dim, int32_t sweeps);
+
 /* max over interior cells of |A u| (Form R) or |f - A u| (Form D), written to
  * *d_out (device double) — kernels.residual_max (kernels.py:254-265).  With
  * batch > 1 the max runs over all grids. */

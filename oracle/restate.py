@@ -93,14 +93,17 @@ def colour_of(name, coord):
     return code
 
 
-def _parity_vectors(dim, colours, colour):
-    """Per-axis parity vectors q (q_a = (c_a-1)&1, a=0 is x) making up `colour`."""
+def _parity_vectors(dim, colours, colour, origin=(0, 0, 0)):
+    """Local per-axis parity vectors q (local c_a = 1 + q_a + 2k, a=0 is x)
+    of the cells of `colour`; colours use GLOBAL coordinates c_a + origin_a
+    (a slab of a larger grid keeps the global colouring)."""
     out = []
     for q in itertools.product((0, 1), repeat=dim):   # q[0] = x parity
+        g = [(q[a] + origin[a]) & 1 for a in range(dim)]
         if colours == 2:
-            c = sum(q) % 2
+            c = sum(g) % 2
         else:
-            c = sum(bit << a for a, bit in enumerate(q))
+            c = sum(bit << a for a, bit in enumerate(g))
         if c == colour:
             out.append(q)
     return out
@@ -112,14 +115,15 @@ def _sl(n, q_axis, shift):
 
 # -- sweeps -------------------------------------------------------------------
 
-def colour_pass(u, name, colour, f=None, omega=None, form="R"):
-    """One colour phase in place on u (shape (..., S, S[, S]))."""
+def colour_pass(u, name, colour, f=None, omega=None, form="R", origin=(0, 0, 0)):
+    """One colour phase in place on u (shape (..., S[, S], S)); the slowest
+    axis may differ in length (slabs)."""
     dim, offsets, weights, wc, colours = STENCIL_TABLE[name]
-    n = u.shape[-1] - 2
+    ns = [u.shape[-1 - a] - 2 for a in range(dim)]   # interior extent per axis (x, y, z)
     lead = (slice(None),) * (u.ndim - dim)
-    for q in _parity_vectors(dim, colours, colour):
+    for q in _parity_vectors(dim, colours, colour, origin):
         # array axes are reversed coordinate axes: [.., z, y, x]
-        centre = lead + tuple(_sl(n, q[a], 0) for a in reversed(range(dim)))
+        centre = lead + tuple(_sl(ns[a], q[a], 0) for a in reversed(range(dim)))
         if u[centre].size == 0:
             continue
         if form == "R":
@@ -127,7 +131,7 @@ def colour_pass(u, name, colour, f=None, omega=None, form="R"):
             for off, w in zip(offsets, weights):
                 if w == 0.0:
                     continue
-                nb = lead + tuple(_sl(n, q[a], off[a]) for a in reversed(range(dim)))
+                nb = lead + tuple(_sl(ns[a], q[a], off[a]) for a in reversed(range(dim)))
                 acc += abs(w) * u[nb]
             out = acc / wc
         elif form == "D":
@@ -136,7 +140,7 @@ def colour_pass(u, name, colour, f=None, omega=None, form="R"):
             for off, w in zip(offsets, weights):
                 if w == 0.0:
                     continue
-                nb = lead + tuple(_sl(n, q[a], off[a]) for a in reversed(range(dim)))
+                nb = lead + tuple(_sl(ns[a], q[a], off[a]) for a in reversed(range(dim)))
                 au = au + w * u[nb]
             out = uc + omega * ((f[centre] - au) / wc)
         else:
@@ -146,12 +150,12 @@ def colour_pass(u, name, colour, f=None, omega=None, form="R"):
         u[centre] = out
 
 
-def sweep(u, name, sweeps=1, f=None, omega=None, form="R"):
+def sweep(u, name, sweeps=1, f=None, omega=None, form="R", origin=(0, 0, 0)):
     """`sweeps` full colour-ordered sweeps in place (strategies.py:371-393)."""
     colours = STENCIL_TABLE[name][4]
     for _ in range(sweeps):
         for c in range(colours):
-            colour_pass(u, name, c, f=f, omega=omega, form=form)
+            colour_pass(u, name, c, f=f, omega=omega, form=form, origin=origin)
     return u
 
 

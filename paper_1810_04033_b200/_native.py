@@ -23,7 +23,7 @@ ABI_VERSION = 1
 # every symbol include/stencil_sweep.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sl_abi_version", "sl_strerror", "sl_last_cuda_error", "sl_launch_count",
            "sl_workspace_bytes",
-           "sl_sweep", "sl_colour_pass", "sl_update_cells", "sl_residual_max")
+           "sl_sweep", "sl_colour_pass", "sl_update_cells", "sl_residual_max", "sl_ghost_depth")
 
 
 class NativeLibraryError(RuntimeError):
@@ -61,6 +61,7 @@ _SIGS = {
                                        ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     "sl_residual_max": (ctypes.c_int, [_P(SlGrid), _P(SlStencil), ctypes.c_void_p,
                                        ctypes.c_void_p]),
+    "sl_ghost_depth": (ctypes.c_int, [_P(SlStencil), ctypes.c_int32, ctypes.c_int32]),
 }
 
 

@@ -9,6 +9,9 @@
 #include "../../include/stencil_sweep.h"
 #include "k1_colour.cuh"
 #include "k2_fused.cuh"
+#include "plan.cuh"
+
+#include <vector>
 
 namespace sl {
 
@@ -125,6 +128,36 @@ static int make_params(const sl_grid *g, const sl_stencil *s, int32_t *d_status,
 
 static bool empty_grid(const Params &p) { return p.nx == 0 || p.ny == 0 || p.nz == 0; }
 
+// Host version of plan.cuh's margin DP for any number of sweeps: the input
+// margin along axis `axis` that `sweeps` fused sweeps of `shape` consume.
+static int load_margin(int shape, int colours, int sweeps, int axis) {
+  const int K = sweeps * colours;
+  const int nnz = shape_nnz(shape);
+  std::vector<int> need(K, -1);
+  for (int c = 0; c < colours; ++c)
+    for (int k = K - 1; k >= 0; --k)
+      if (k % colours == c) {
+        need[k] = 0;
+        break;
+      }
+  int load = 0;
+  for (int j = K - 1; j >= 0; --j) {
+    if (need[j] < 0) continue;
+    for (int q = 0; q < nnz; ++q) {
+      const Off o = shape_off(shape, q);
+      const int b = (j % colours) ^ colour_flip(colours, o);
+      int i = j - 1;
+      while (i >= 0 && i % colours != b) --i;
+      const int req = need[j] + cabs(off_axis(o, axis));
+      if (i >= 0)
+        need[i] = cmax(need[i], req);
+      else
+        load = cmax(load, req);
+    }
+  }
+  return load;
+}
+
 }  // namespace sl
 
 using namespace sl;
@@ -203,6 +236,16 @@ int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flat
   if (rc != SL_OK) return rc;
   if (!d_status || count < 0 || (count > 0 && !d_flats)) return SL_E_INVAL;
   return cuda_status(launch_update_cells(key, p, d_flats, count, (cudaStream_t)stream));
+}
+
+int sl_ghost_depth(const sl_stencil *s, int32_t dim, int32_t sweeps) {
+  if (!s || (dim != 2 && dim != 3) || sweeps < 0) return -SL_E_INVAL;
+  KernelKey key;
+  Params p;
+  std::memset(&p, 0, sizeof(p));
+  if (resolve(s, dim, &key, &p) != SL_OK) return -SL_E_INVAL;
+  if (sweeps == 0) return 0;
+  return load_margin(key.shape, s->colours, sweeps, dim - 1);
 }
 
 int sl_residual_max(const sl_grid *g, const sl_stencil *s, double *d_out, void *stream) {

@@ -1,0 +1,66 @@
+"""Slab kernels on the GPU: several slabs of one grid emulated on one device.
+
+The exchange is done with device-to-device copies mirroring
+SlabRunner.exchange (one process, so no NCCL rendezvous is needed); this
+checks the fused kernels with odd slab origins and ghost depths.  The NCCL
+P2P path itself is covered on CPU with gloo (tests/test_slabs.py).
+"""
+
+import numpy as np
+import pytest
+
+import paper_1810_04033_b200 as sl
+from oracle import coracle
+from oracle import restate as R
+from paper_1810_04033_b200.slabs import SlabRunner
+
+pytestmark = pytest.mark.gpu
+
+
+def _emulated(name, n, sweeps, world, per):
+    kind = sl.get_stencil(name)
+    rs = [SlabRunner(kind.dim, n, kind, world=world, rank=r, ghost_sweeps=per, device="cuda")
+          for r in range(world)]
+    for r in rs:
+        r.init(7, 8, 0.8)
+    left = sweeps
+    while left > 0:
+        k = min(per, left)
+        for r in rs:
+            r._compute(k)
+        left -= k
+        for r0, r1 in zip(rs, rs[1:]):   # what exchange() sends, as device copies
+            L0, L1, G = r0.layout, r1.layout, r0.layout.ghost
+            r1.u[0:L1.a - L1.lo].copy_(r0.u[L1.lo - L0.lo:L1.a - L0.lo])
+            r0.u[L0.b + 1 - L0.lo:].copy_(r1.u[L0.b + 1 - L1.lo:L0.hi + 1 - L1.lo])
+    for r in rs:
+        r.check_status()
+    out = np.zeros((n + 2,) * kind.dim)
+    for i, r in enumerate(rs):
+        L = r.layout
+        lo = 0 if i == 0 else L.a
+        hi = n + 1 if i == world - 1 else L.b
+        out[lo:hi + 1] = r.u[lo - L.lo:hi + 1 - L.lo].cpu().numpy()
+    return out
+
+
+@pytest.mark.parametrize("name,n,sweeps,world,per", [
+    ("fd7", 40, 5, 2, 1), ("fd7", 37, 4, 3, 2), ("fe27q1", 30, 3, 2, 1),
+    ("fe9", 130, 4, 2, 1), ("fe9", 97, 5, 3, 2), ("fd5", 66, 6, 2, 2)])
+def test_emulated_slabs_equal_single_domain(name, n, sweeps, world, per):
+    dim = R.STENCIL_TABLE[name][0]
+    want = R.init_u(dim, n, 7)
+    f = R.init_f(dim, n, 8)
+    coracle.sweep(want, name, sweeps, f=f, omega=0.8, form="D")
+    got = _emulated(name, n, sweeps, world, per)
+    assert np.array_equal(got.view(np.int64), want.view(np.int64))
+
+
+def test_single_rank_slab_runner():
+    kind = sl.FD7
+    r = SlabRunner(3, 24, kind, device="cuda")
+    r.init(7, 8, 0.8)
+    r.sweep(3)
+    want = R.init_u(3, 24, 7)
+    coracle.sweep(want, "fd7", 3, f=R.init_f(3, 24, 8), omega=0.8, form="D")
+    assert np.array_equal(r.gather().view(np.int64), want.view(np.int64))
