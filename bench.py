@@ -237,6 +237,7 @@ def flush_l2(torch, buf):
 
 
 def run_ours(args, wl, rank, world, local):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -250,11 +251,23 @@ def run_ours(args, wl, rank, world, local):
     flags = _native.SL_FLAG_PER_COLOUR if args.per_colour else 0
 
     cost = sl.CostModel()
+    total_updates = wl.updates * world          # replicas (config 1): every rank does the grid
+    scaling, parallelism = "weak", ("single-gpu" if world == 1 else f"replicas x{world}")
+    h2d_bytes = 2 * wl.grid_elems * 8
+    d2h_bytes = wl.grid_elems * 8
     if wl.batch > 1:
+        # config 5: the patches are split evenly across ranks (no exchange)
+        lo, hi = rank * wl.batch // world, (rank + 1) * wl.batch // world
         u0, f0 = sl.init_patches(wl.batch, wl.n, wl.seed)
-        pinned_u = torch.from_numpy(u0).pin_memory()
-        pinned_f = torch.from_numpy(f0).pin_memory()
+        pinned_u = torch.from_numpy(np.ascontiguousarray(u0[lo:hi])).pin_memory()
+        pinned_f = torch.from_numpy(np.ascontiguousarray(f0[lo:hi])).pin_memory()
+        del u0, f0
         pb = sl.PatchBatch(pinned_u, pinned_f, wl.omega, device=dev)
+        pinned_out = torch.empty_like(pinned_u).pin_memory()
+        if world > 1:
+            total_updates, scaling, parallelism = wl.updates, "strong", f"patches split x{world}"
+            h2d_bytes = 2 * pinned_u.numel() * 8
+            d2h_bytes = pinned_u.numel() * 8
 
         def step():
             pb.sweep(kind, wl.sweeps, flags=flags)
@@ -262,13 +275,36 @@ def run_ours(args, wl, rank, world, local):
         def e2e_prep():
             pass
 
-        pinned_out = torch.empty_like(pinned_u).pin_memory()
-
         def e2e_step():
             # the public calls a user makes: host patches in, swept patches out
             pb.upload(pinned_u, pinned_f)
             pb.sweep(kind, wl.sweeps, flags=flags)
             return pb.values(out=pinned_out)
+    elif world > 1 and wl.index in (2, 3, 4):
+        # configs 2-4: slabs along the slowest axis, ghost planes exchanged by NCCL P2P
+        from paper_1810_04033_b200.slabs import SlabRunner
+        sr = SlabRunner(wl.dim, wl.n, kind, world=world, rank=rank, ghost_sweeps=1, device=dev)
+        sr.init(wl.seed, wl.seed + 1, wl.omega)
+        total_updates, scaling = wl.updates, "strong"
+        parallelism = f"slabs x{world} (axis {'z' if wl.dim == 3 else 'y'}, ghost {sr.layout.ghost}, NCCL P2P)"
+        u_host = sr.u.cpu().pin_memory()
+        f_host = sr.f.cpu().pin_memory()
+        out_host = torch.empty_like(sr.owned()).cpu().pin_memory()
+        h2d_bytes = 2 * u_host.numel() * 8
+        d2h_bytes = out_host.numel() * 8
+
+        def step():
+            sr.sweep(wl.sweeps)
+
+        def e2e_prep():
+            pass
+
+        def e2e_step():
+            sr.u.copy_(u_host, non_blocking=True)
+            sr.f.copy_(f_host, non_blocking=True)
+            sr.sweep(wl.sweeps)
+            out_host.copy_(sr.owned())
+            return out_host
     else:
         mesh = sl.Mesh(wl.dim, wl.n, device=dev)
         sl.init(mesh, wl.seed)
@@ -322,7 +358,7 @@ def run_ours(args, wl, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * wl.updates / (ms_per_step / 1e3) / 1e9
+    value = total_updates / (ms_per_step / 1e3) / 1e9
 
     # end to end through the public API with host buffers (pinned)
     e2e = None
@@ -341,19 +377,20 @@ def run_ours(args, wl, rank, world, local):
         te = torch.tensor([sum(e2e_times) / len(e2e_times)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * wl.updates / float(te.item()) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * grid_bytes, "d2h_bytes_per_step": grid_bytes}
+        e2e = {"value": total_updates / float(te.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes}
 
     if rank != 0:
         return
     peak, peak_src = peaks()
-    achieved = BYTES_PER_UPDATE * wl.updates / (ms_per_step / 1e3) / 1e9   # one rank's kernel
+    achieved = BYTES_PER_UPDATE * total_updates / world / (ms_per_step / 1e3) / 1e9   # per GPU
     per_step_launches = launches / args.steps
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded U[0,1) u0, U[-1,1) f)",
-            "config": workload_config(wl, world, {"path": "k1-per-colour" if args.per_colour else "auto"}),
+            "config": workload_config(wl, world, {"path": "k1-per-colour" if args.per_colour else "auto",
+                                                  "parallelism": parallelism}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(wl.name),
                          "peak_source": peak_src,
