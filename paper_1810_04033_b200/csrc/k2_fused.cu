@@ -502,10 +502,19 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
   double *bufs[2] = {p.u, workspace};
   int cur = 0;
   cudaError_t e = cudaSuccess;
-  for (int s = 0; s < sweeps && e == cudaSuccess; ++s) {
+  // FD5 (red-black 2D) fuses two sweeps per pass: half the passes, and the
+  // 2-sweep ghost (4 columns/rows) still fits a 64-column strip
+  const bool two = key.shape == FD5 && sweeps >= 2;
+  for (int s = 0; s < sweeps && e == cudaSuccess;) {
+    const int m = (two && sweeps - s >= 2) ? 2 : 1;
     e = dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
-      return launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
+      if constexpr (S == FD5)
+        return m == 2 ? launch_pass<S, F, U, D, 2>(p, bufs[cur], bufs[cur ^ 1], st)
+                      : launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
+      else
+        return launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
     });
+    s += m;
     cur ^= 1;
   }
   if (e == cudaSuccess && cur == 1) {
