@@ -61,6 +61,8 @@ enum sl_form { SL_FORM_R = 0, SL_FORM_D = 1 };
 #define SL_FLAG_PER_COLOUR 0x1u   /* one in-place launch per colour phase (K1), no fusion */
 #define SL_FLAG_MERGE_COLOURS 0x2u /* negative control: all colours in ONE racy pass
                                       (reference _fault_merge_colours, strategies.py:364-369) */
+#define SL_FLAG_STREAM 0x4u        /* fused path: always the streaming kernels (no small-grid
+                                      tile kernel, no on-chip patch kernel) — for testing */
 
 typedef struct sl_grid {
     int32_t dim;              /* 2 or 3 */

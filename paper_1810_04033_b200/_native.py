@@ -18,6 +18,7 @@ SL_FD5, SL_FE9, SL_FD7, SL_FE27 = 0, 1, 2, 3
 SL_FORM_R, SL_FORM_D = 0, 1
 SL_FLAG_PER_COLOUR = 0x1
 SL_FLAG_MERGE_COLOURS = 0x2
+SL_FLAG_STREAM = 0x4
 ABI_VERSION = 1
 
 # every symbol include/stencil_sweep.h declares (checked by tests/test_abi.py)

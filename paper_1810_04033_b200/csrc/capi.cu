@@ -217,7 +217,8 @@ int sl_sweep(const sl_grid *g, const sl_stencil *s, int32_t sweeps, uint32_t fla
   }
   if (!(flags & SL_FLAG_PER_COLOUR)) {
     int handled = 0;
-    rc = cuda_status(launch_fused(key, p, sweeps, workspace, workspace_bytes, st, &handled));
+    rc = cuda_status(launch_fused(key, p, sweeps, workspace, workspace_bytes, st, &handled,
+                                  (flags & SL_FLAG_STREAM) != 0));
     if (rc != SL_OK || handled) return rc;
   }
   for (int i = 0; i < sweeps; ++i)

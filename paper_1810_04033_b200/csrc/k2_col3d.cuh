@@ -238,8 +238,11 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
 #pragma unroll
                 for (int r = 0; r < G::RT; ++r)
                   if (own_out[r]) {
-                    bad |= ((((unsigned)__double2hiint(U[r][SM2][0]) & 0x7ff00000u) == 0x7ff00000u) |
-                            (((unsigned)__double2hiint(U[r][SM2][1]) & 0x7ff00000u) == 0x7ff00000u));
+                    const bool in_yz = pz >= 1 && pz <= nz && gy[r] >= 1 && gy[r] <= ny;
+                    bad |= (in_yz && gx >= 1 &&
+                            ((unsigned)__double2hiint(U[r][SM2][0]) & 0x7ff00000u) == 0x7ff00000u) |
+                           (in_yz && gx + 1 <= nx &&
+                            ((unsigned)__double2hiint(U[r][SM2][1]) & 0x7ff00000u) == 0x7ff00000u);
                     stg_pair(dst + (int64_t)pz * p.sz + (int64_t)gy[r] * p.sy + gx, U[r][SM2][0], U[r][SM2][1]);
                   }
               }

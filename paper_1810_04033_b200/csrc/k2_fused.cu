@@ -308,6 +308,13 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
   if (bad) atomicOr(p.status, 1);
 }
 
+}  // namespace sl
+
+// K4 (small 2D grids) reuses update_item / xoff / stg2 above
+#include "k4_block2d.cuh"
+
+namespace sl {
+
 // ---------------------------------------------------------------------------
 // host side
 
@@ -486,10 +493,32 @@ static cudaError_t launch_patches(const KernelKey &key, const Params &p, int swe
   return e;
 }
 
+// K4: 2D grids small enough to be L2-resident run M sweeps per pass in
+// shared-memory tiles (one wave of 1024-thread CTAs).
+static bool block2d_preferred(const KernelKey &key, const Params &p) {
+  return shape_dim(key.shape) == 2 && (p.nx + 2) * (p.ny + 2) <= (int64_t)4 * 1024 * 1024;
+}
+
+template <int S, int FORM, bool UNIT, int DIV, int M>
+static cudaError_t launch_block2d(const Params &p, const double *src, double *dst, cudaStream_t st) {
+  using G = GeoB2<S, M>;
+  auto kern = k4_block2d<S, FORM, UNIT, DIV, M>;
+  static thread_local int64_t slots = 0;
+  if (!slots) {
+    cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t Sx = p.nx + 2, Sy = p.ny + 2;
+  const int ntx = (int)((Sx + G::TX - 1) / G::TX), nty = (int)((Sy + G::TY - 1) / G::TY);
+  kern<<<(unsigned)(ntx * nty), G::NT, G::SMEM, st>>>(p, src, dst, ntx, nty);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, double *workspace,
-                         size_t workspace_bytes, cudaStream_t st, int *handled) {
+                         size_t workspace_bytes, cudaStream_t st, int *handled, bool stream_only) {
   *handled = 0;
-  if (p.batch > 1 || (p.nx == 16 && p.ny == 16 && shape_dim(key.shape) == 2)) {
+  if (p.batch > 1 || (!stream_only && p.nx == 16 && p.ny == 16 && shape_dim(key.shape) == 2)) {
     if (!patch_supported(key, p)) return cudaSuccess;
     *handled = 1;
     return launch_patches(key, p, sweeps, st);
@@ -502,6 +531,30 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
   double *bufs[2] = {p.u, workspace};
   int cur = 0;
   cudaError_t e = cudaSuccess;
+  if (!stream_only && block2d_preferred(key, p)) {
+    // FD5: 4 sweeps per pass, FE9: 2 (ghost 8 columns); remainder 1 at a time
+    const int mk = key.shape == FD5 ? 4 : 2;
+    for (int s = 0; s < sweeps && e == cudaSuccess;) {
+      const int m = sweeps - s >= mk ? mk : 1;
+      e = dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
+        if constexpr (S == FD5)
+          return m == 4 ? launch_block2d<S, F, U, D, 4>(p, bufs[cur], bufs[cur ^ 1], st)
+                        : launch_block2d<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
+        else if constexpr (S == FE9)
+          return m == 2 ? launch_block2d<S, F, U, D, 2>(p, bufs[cur], bufs[cur ^ 1], st)
+                        : launch_block2d<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
+        else
+          return cudaErrorInvalidValue;
+      });
+      s += m;
+      cur ^= 1;
+    }
+    if (e == cudaSuccess && cur == 1) {
+      e = cudaMemcpyAsync(p.u, workspace, need, cudaMemcpyDeviceToDevice, st);
+      note_launch();
+    }
+    return e;
+  }
   // FD5 (red-black 2D) fuses two sweeps per pass: half the passes, and the
   // 2-sweep ghost (4 columns/rows) still fits a 64-column strip
   const bool two = key.shape == FD5 && sweeps >= 2;

@@ -262,8 +262,11 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                     const double a = uu[RO][2 * k], b = uu[RO][2 * k + 1];
                     // non-finite results are sticky through later updates, so
                     // checking each owned value once, when final, catches them
-                    bad |= (((unsigned)__double2hiint(a) & 0x7ff00000u) == 0x7ff00000u) |
-                           (((unsigned)__double2hiint(b) & 0x7ff00000u) == 0x7ff00000u);
+                    const bool in_y = row >= 1 && row <= ny;
+                    bad |= (in_y && gx + 2 * k >= 1 &&
+                            ((unsigned)__double2hiint(a) & 0x7ff00000u) == 0x7ff00000u) |
+                           (in_y && gx + 2 * k + 1 <= nx &&
+                            ((unsigned)__double2hiint(b) & 0x7ff00000u) == 0x7ff00000u);
                     stg_pair(dst + (int64_t)row * p.sy + gx + 2 * k, a, b);
                   }
                 }

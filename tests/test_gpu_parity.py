@@ -97,6 +97,8 @@ def _gpu_d(name, n, sweeps, seed=42, boundary=0.0, mode="fused"):
         sl.run_sweeps(m, kind, sl.CostModel(), sweeps)
     elif mode == "k1":
         sl.run_sweeps(m, kind, sl.CostModel(), sweeps, flags=_native.SL_FLAG_PER_COLOUR)
+    elif mode == "stream":
+        sl.run_sweeps(m, kind, sl.CostModel(), sweeps, flags=_native.SL_FLAG_STREAM)
     else:
         for _ in range(sweeps):
             sl.sweep_colouring(sl.DevicePool(), m, kind, sl.CostModel())
@@ -104,12 +106,12 @@ def _gpu_d(name, n, sweeps, seed=42, boundary=0.0, mode="fused"):
 
 
 @pytest.mark.parametrize("name", ALL)
-@pytest.mark.parametrize("mode", ["fused", "k1", "single"])
+@pytest.mark.parametrize("mode", ["fused", "stream", "k1", "single"])
 def test_form_d_matches_oracle_small_and_ragged(name, mode):
     dim = R.STENCIL_TABLE[name][0]
     sizes = (1, 2, 3, 7, 16, 33, 64, 130) if dim == 2 else (1, 2, 3, 5, 8, 17, 32)
     for n in sizes:
-        for sweeps in (1, 2, 5):
+        for sweeps in (1, 2, 5, 9):
             want = _oracle_d(name, n, sweeps, seed=n)
             got = _gpu_d(name, n, sweeps, seed=n, mode=mode)
             assert _bits_equal(got, want), (name, n, sweeps, mode)
@@ -239,7 +241,7 @@ def test_merged_colour_negative_control_mismatches():
 
 def test_deterministic_across_repeats_and_paths():
     digests = set()
-    for mode in ("fused", "k1", "single", "fused"):
+    for mode in ("fused", "stream", "k1", "single", "fused"):
         digests.add(_digest(_gpu_d("fe27q1", 20, 3, mode=mode)))
     assert len(digests) == 1
 
