@@ -90,7 +90,8 @@ struct Geo3 {
   static constexpr int NW = NT / 32;
   static constexpr int PAIRS = PY * PX / 2;
   static constexpr int LPT = PAIRS / NT;
-  static constexpr size_t SMEM = size_t(W * SLOT + PAD_ROWS * ROWW) * sizeof(double);
+  static constexpr int LEAD = 2;             // item reads may start one row before a slot
+  static constexpr size_t SMEM = size_t(W * SLOT + (PAD_ROWS + LEAD) * ROWW) * sizeof(double);
   static_assert(PAIRS % NT == 0, "plane load split");
   static_assert(TX >= 8 && TY >= 4, "ghost margin too wide for the tile");
   static_assert(SMEM <= 227 * 1024, "window exceeds shared memory");
@@ -222,7 +223,7 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
   const int zlim = z1 + G::GZ;
   int so[G::W];  // so[k] = smem offset of the slot holding plane t+1-k (rotated per step)
 #pragma unroll
-  for (int k = 0; k < G::W; ++k) so[k] = (((t_begin + 1 - k) % G::W + G::W) % G::W) * G::SLOT;
+  for (int k = 0; k < G::W; ++k) so[k] = (((t_begin + 1 - k) % G::W + G::W) % G::W) * G::SLOT + G::LEAD * G::ROWW;
   double2 pu[G::LPT];
   load_regs(src, t_begin + 1, pu);
 

@@ -33,9 +33,11 @@ struct GeoB2 {
   static constexpr int RY = 2;
   static constexpr int NT = 1024;
   static constexpr int NW = NT / 32;
-  static constexpr int PAD_ROWS = (RY - 1) * RSTEP + 2;
-  static constexpr int FOFF = (PY + PAD_ROWS) * ROWW;
-  static constexpr size_t SMEM = size_t(2 * (PY + PAD_ROWS) * ROWW) * sizeof(double);
+  static constexpr int PAD_ROWS = (RY - 1) * RSTEP + 2;   // items may read past the last row
+  static constexpr int LEAD = 2;                          // ... and one row before the first
+  static constexpr int UOFF = LEAD * ROWW;
+  static constexpr int FOFF = UOFF + (PY + PAD_ROWS + LEAD) * ROWW;
+  static constexpr size_t SMEM = size_t(2 * (PY + PAD_ROWS + LEAD) * ROWW) * sizeof(double);
   static_assert(SMEM <= 227 * 1024, "tile exceeds shared memory");
 };
 
@@ -65,8 +67,8 @@ k4_block2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
       u2 = *reinterpret_cast<const double2 *>(src + (int64_t)gy * sy + gx);
       if (FORM == 1) f2 = __ldg(reinterpret_cast<const double2 *>(p.f + (int64_t)gy * sy + gx));
     }
-    sm[r * G::ROWW + 1 + i] = u2.x;
-    sm[r * G::ROWW + G::HW + 1 + i] = u2.y;
+    sm[G::UOFF + r * G::ROWW + 1 + i] = u2.x;
+    sm[G::UOFF + r * G::ROWW + G::HW + 1 + i] = u2.y;
     if (FORM == 1) {
       sm[G::FOFF + r * G::ROWW + 1 + i] = f2.x;
       sm[G::FOFF + r * G::ROWW + G::HW + 1 + i] = f2.y;
@@ -105,10 +107,10 @@ k4_block2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
               const bool v = row >= r_first && row < r_hi && lx >= lx_lo && lx < lx_hi && gx >= 1 && gx <= nx;
               vmask |= (unsigned)v << r;
             }
-            const int rb = (row0 - 1) * G::ROWW + li;
+            const int rb = G::UOFF + (row0 - 1) * G::ROWW + li;
             auto ro = [&](int, int k) -> int { return rb + k * G::ROWW; };
             auto fv = [&](int r, int s) -> double {
-              return sm[G::FOFF + rb + (r * G::RSTEP + 1) * G::ROWW + xoff<G::HW>(s, 0)];
+              return sm[G::FOFF - G::UOFF + rb + (r * G::RSTEP + 1) * G::ROWW + xoff<G::HW>(s, 0)];
             };
             bad |= update_item<S, FORM, UNIT, DIV, G::RY, G::RSTEP, G::RB, G::HW, S0>(ro, fv, vmask, p);
           }
@@ -120,7 +122,7 @@ k4_block2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
   // ---- owned part -> dst ----
   for (int k = tid; k < TYo * (TXo / 2); k += G::NT) {
     const int r = G::GY + k / (TXo / 2), i = G::GX / 2 + k % (TXo / 2);
-    const double a = sm[r * G::ROWW + 1 + i], b = sm[r * G::ROWW + G::HW + 1 + i];
+    const double a = sm[G::UOFF + r * G::ROWW + 1 + i], b = sm[G::UOFF + r * G::ROWW + G::HW + 1 + i];
     // (non-finite updates were flagged by update_item as they happened)
     stg2(dst + (int64_t)(gy0 + r) * sy + gx0 + 2 * i, a, b);
   }
