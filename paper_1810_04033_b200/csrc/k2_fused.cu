@@ -27,6 +27,7 @@
 #include "k2_strip2d.cuh"
 #include "k3_patch.cuh"
 #include "k2_col3d.cuh"
+#include "k2_q1col.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -400,7 +401,8 @@ static cudaError_t prepare(Kern kern, size_t smem, int threads, int64_t *slots) 
 }
 
 // 3D fp64 tensor map over a dense (n+2)^3 grid with a 64 x 32 x 1 box.
-static cudaError_t make_tmap3(CUtensorMap *map, const double *base, const Params &p) {
+static cudaError_t make_tmap3(CUtensorMap *map, const double *base, const Params &p,
+                              int boxx = Col3Geo::PX, int boxy = Col3Geo::PY) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -411,7 +413,7 @@ static cudaError_t make_tmap3(CUtensorMap *map, const double *base, const Params
   }
   const cuuint64_t dims[3] = {(cuuint64_t)(p.nx + 2), (cuuint64_t)(p.ny + 2), (cuuint64_t)(p.nz + 2)};
   const cuuint64_t strides[2] = {(cuuint64_t)p.sy * 8, (cuuint64_t)p.sz * 8};
-  const cuuint32_t box[3] = {(cuuint32_t)Col3Geo::PX, (cuuint32_t)Col3Geo::PY, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)boxx, (cuuint32_t)boxy, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides,
                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -437,6 +439,23 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     const int64_t ntx = (Sx + G::TX - 1) / G::TX, nty = (Sy + G::TY - 1) / G::TY;
     const int64_t nzc = pick_chunks(ntx * nty, Sz, slots, G::GZ + G::LAGMAX + G::R, 16);
     kern<<<(unsigned)(ntx * nty * nzc), G::NT, G::SMEM, st>>>(p, tmu, tmf, dst, ntx, nty, nzc);
+    note_launch();
+    return cudaGetLastError();
+  } else if constexpr (S == Q1 && M == 1) {
+    using G = Q1Geo;
+    auto kern = k2_q1col<FORM, UNIT, DIV>;
+    static thread_local int64_t slots = 0;
+    if (!slots) {
+      cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
+      if (e != cudaSuccess) return e;
+    }
+    CUtensorMap tmu;
+    cudaError_t e = make_tmap3(&tmu, src, p, G::PX, G::BOXY);
+    if (e != cudaSuccess) return e;
+    const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
+    const int64_t ntx = (Sx + G::TX - 1) / G::TX, nty = (Sy + G::TY - 1) / G::TY;
+    const int64_t nzc = pick_chunks(ntx * nty, Sz, slots, G::GZ + G::LAGMAX + G::RR, 16);
+    kern<<<(unsigned)(ntx * nty * nzc), G::NT, G::SMEM, st>>>(p, tmu, dst, ntx, nty, nzc);
     note_launch();
     return cudaGetLastError();
   } else if constexpr (shape_dim(S) == 3) {

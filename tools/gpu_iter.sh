@@ -10,7 +10,7 @@ for c in 2 3 4 1; do
 done
 for c in "$@"; do
   python tools/prof_run.py --config $c --sweeps 2 > gpurun_out/plain$c.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k2_ -s 1 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:k[1-4]_ -s 1 -c 1 \
       -o gpurun_out/prof_c$c python tools/prof_run.py --config $c --sweeps 2 > gpurun_out/ncu$c.log 2>&1
 done
 tail -n 2 gpurun_out/pytest_gpu.log
