@@ -422,6 +422,36 @@ static cudaError_t make_tmap3(CUtensorMap *map, const double *base, const Params
 }
 
 template <int S, int FORM, bool UNIT, int DIV, int M>
+static cudaError_t launch_stream3d(const Params &p, const double *src, double *dst, cudaStream_t st) {
+    using G = Geo3<S, M>;
+    auto kern = k2_stream3d<S, FORM, UNIT, DIV, M>;
+    static thread_local int64_t slots = 0;
+    if (!slots) {
+      cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
+      if (e != cudaSuccess) return e;
+    }
+    Tiles tl;
+    const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
+    tl.ntx = (Sx + G::TX - 1) / G::TX;
+    tl.nty = (Sy + G::TY - 1) / G::TY;
+    tl.nzc = pick_chunks(tl.ntx * tl.nty, Sz, slots, G::GZ + G::LAGMAX + 1, 16);
+    const int64_t items = tl.ntx * tl.nty * tl.nzc;
+    kern<<<(unsigned)items, G::NT, G::SMEM, st>>>(p, src, dst, tl);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// k2_q1col holds the Q1 weights as two values: all edges equal, all corners equal
+static bool q1_two_weights(const Params &p) {
+  for (int j = 0; j < shape_nnz(Q1); ++j) {
+    const Off o = shape_off(Q1, j);
+    const bool corner = o.x != 0 && o.y != 0 && o.z != 0;
+    if (p.w[j] != (corner ? p.w[0] : p.w[1])) return false;
+  }
+  return true;
+}
+
+template <int S, int FORM, bool UNIT, int DIV, int M>
 static cudaError_t launch_pass(const Params &p, const double *src, double *dst, cudaStream_t st) {
   if constexpr (S == FD7 && M == 1) {
     using G = Col3Geo;
@@ -442,6 +472,7 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     note_launch();
     return cudaGetLastError();
   } else if constexpr (S == Q1 && M == 1) {
+    if (!q1_two_weights(p)) return launch_stream3d<S, FORM, UNIT, DIV, M>(p, src, dst, st);
     using G = Q1Geo;
     auto kern = k2_q1col<FORM, UNIT, DIV>;
     static thread_local int64_t slots = 0;
@@ -459,22 +490,7 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     note_launch();
     return cudaGetLastError();
   } else if constexpr (shape_dim(S) == 3) {
-    using G = Geo3<S, M>;
-    auto kern = k2_stream3d<S, FORM, UNIT, DIV, M>;
-    static thread_local int64_t slots = 0;
-    if (!slots) {
-      cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
-      if (e != cudaSuccess) return e;
-    }
-    Tiles tl;
-    const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
-    tl.ntx = (Sx + G::TX - 1) / G::TX;
-    tl.nty = (Sy + G::TY - 1) / G::TY;
-    tl.nzc = pick_chunks(tl.ntx * tl.nty, Sz, slots, G::GZ + G::LAGMAX + 1, 16);
-    const int64_t items = tl.ntx * tl.nty * tl.nzc;
-    kern<<<(unsigned)items, G::NT, G::SMEM, st>>>(p, src, dst, tl);
-    note_launch();
-    return cudaGetLastError();
+    return launch_stream3d<S, FORM, UNIT, DIV, M>(p, src, dst, st);
   } else {
     using G = GeoS2<S, M>;
     auto kern = k2_strip2d<S, FORM, UNIT, DIV, M>;

@@ -141,6 +141,8 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   load_f(t_begin, fcur);
 
   const int lrow0 = r0 * G::PX + 2 * lane;  // element offset of (row r0, col 2*lane) in a slot
+  // compact Q1 order: index 0 = (-1,-1,-1) corner, 1 = (0,-1,-1) edge
+  const double wC = p.w[0], wE = p.w[1], awC = p.aw[0], awE = p.aw[1];
   unsigned bad = 0;
   for (int t0 = t_begin; t0 <= t_end; t0 += RR) {
     [&]<int... Ks>(std::integer_sequence<int, Ks...>) {
@@ -211,8 +213,13 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
                       for (int q = 0; q < shape_nnz(Q1); ++q) {
                         const Off o = shape_off(Q1, q);
                         if (o.z != dz) continue;
-                        acc0 = acc_add<FORM, UNIT>(acc0, w[o.y + 1][o.x + 1], q, p);
-                        acc1 = acc_add<FORM, UNIT>(acc1, w[o.y + 1][o.x + 2], q, p);
+                        // Q1 weights take two values (edges, corners; checked on the
+                        // host), held in two registers instead of 20 parameters
+                        const bool corner = o.x != 0 && o.y != 0 && o.z != 0;
+                        const double wq = FORM == 0 ? (corner ? awC : awE) : (corner ? wC : wE);
+                        const double v0 = w[o.y + 1][o.x + 1], v1 = w[o.y + 1][o.x + 2];
+                        acc0 = __dadd_rn(acc0, __dmul_rn(wq, v0));
+                        acc1 = __dadd_rn(acc1, __dmul_rn(wq, v1));
                       }
                     }
                     const double2 fc = fcur[GI];
