@@ -45,17 +45,19 @@ __host__ __device__ constexpr int off_axis(Off o, int a) { return a == 0 ? o.x :
 // Is colour a's point adjacent (through a non-zero offset with o.z == dz) to
 // a colour-b point?
 __host__ __device__ constexpr bool reads_at(int shape, int colours, int a, int b, int dz) {
+  const int sa = shape_dim(shape) - 1;  // streaming axis
   for (int q = 0; q < shape_nnz(shape); ++q) {
     const Off o = shape_off(shape, q);
-    if (o.z == dz && (a ^ colour_flip(colours, o)) == b) return true;
+    if (off_axis(o, sa) == dz && (a ^ colour_flip(colours, o)) == b) return true;
   }
   return false;
 }
 
-// spread = true (3D CTA kernel): additionally delay a phase until it cannot
-// touch any phase processed in the same step — it neither reads a plane an
-// earlier same-step phase writes nor writes one it reads — so all phases of
-// a step run concurrently between two block barriers.  With 2^d colours a
+// spread = true: additionally delay a phase until it cannot touch any phase
+// processed in the same step — it neither reads a plane an earlier same-step
+// phase writes nor writes one it reads — so all phases of a step are
+// independent (3D CTA kernels: one block barrier per step; 2D warp strips:
+// independent dependency chains the scheduler can interleave).  With 2^d colours a
 // colour lives on planes of one parity, so two phases whose lags differ by
 // the wrong parity are never active in the same step and cannot conflict.
 __host__ __device__ constexpr FPlan make_plan(int shape, int colours, int m, bool spread = false) {
@@ -84,8 +86,9 @@ __host__ __device__ constexpr FPlan make_plan(int shape, int colours, int m, boo
         for (int i = 0; i < j; ++i) {
           const int d = L - P.lag[i];
           if (d < -1 || d > 1) continue;
-          const int qi = (P.colour[i] >> 2) & 1, qj = (P.colour[j] >> 2) & 1;
-          const bool coactive = colours == 2 || dim == 2 || (((d - (qi - qj)) & 1) == 0);
+          // a 2^d colour lives on planes (rows in 2D) of one parity along the streaming axis
+          const int qi = (P.colour[i] >> sa) & 1, qj = (P.colour[j] >> sa) & 1;
+          const bool coactive = colours == 2 || (((d - (qi - qj)) & 1) == 0);
           if (coactive && reads_at(shape, colours, P.colour[j], P.colour[i], d)) {
             ++L;
             moved = true;
