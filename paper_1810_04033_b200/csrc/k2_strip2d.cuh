@@ -8,13 +8,12 @@
 // boundary, from the adjacent lane by one warp shuffle.
 //
 // Memory path: each warp has a private ring of NS row slots in shared
-// memory (u row segment + f row segment).  Lane 0 keeps the ring full with
-// TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx) — one copy per
-// array per row, no registers held while in flight.  At step t the warp
-// waits on row t+1's mbarrier and moves the lane's u pair into a small
-// register ring (rows t-LAGMAX-1 .. t+1); f is read from the slot when a
-// phase needs it, so a slot is re-armed (row r -> row r+NS) only after row
-// r's last phase, at step r+LAGMAX.
+// memory (u row segment + f row segment).  Lane 0 keeps NS rows in
+// flight with TMA bulk copies (cp.async.bulk ... mbarrier::complete_tx) —
+// one copy per array per row, no registers held while in flight.
+// At step t the warp waits on row t+1's mbarrier, moves the lane's pair into
+// a small register ring (rows t-LAGMAX-1 .. t+1) and re-arms the slot for
+// row t+1+NS.
 //
 // Phase k processes row t - lag[k] at step t (plan.cuh).  The step loop is
 // unrolled by U (a multiple of both ring lengths) with the row parity of
@@ -29,9 +28,7 @@ namespace sl {
 
 template <int S, int M>
 struct GeoS2 {
-  // FE9: spread lags {0,1,3,4} -> each step runs two independent phases
-  static constexpr bool SPREAD = (S == FE9 && M == 1);
-  static constexpr FPlan P = make_plan(S, S == FE9 ? 4 : 2, M, SPREAD);
+  static constexpr FPlan P = make_plan(S, S == FE9 ? 4 : 2, M);
   static constexpr int K = P.K, C = P.C, LAGMAX = P.lagmax;
   static constexpr bool RB = (P.C == 2);
   static constexpr int GX = (P.load[0] + 1) & ~1;
@@ -41,7 +38,7 @@ struct GeoS2 {
   static constexpr int TX = WS - 2 * GX;
   static constexpr int NRR0 = LAGMAX + 3;             // register ring: rows t-LAGMAX-1 .. t+1
   static constexpr int NRR = NRR0 <= 2 ? 2 : (NRR0 <= 4 ? 4 : 8);
-  static constexpr int NS = 16;                        // smem ring slots: rows t-LAGMAX .. (in flight)
+  static constexpr int NS = 8;                         // smem ring slots (rows in flight)
   static constexpr int U = NRR > NS ? NRR : NS;        // unroll: multiple of both (powers of 2)
   static constexpr int WPB = 2;                        // warps per block
   static constexpr int ROWB = WS * 8;                  // bytes of one array's row segment
@@ -147,10 +144,8 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
 #pragma unroll
     for (int s = 0; s < NS; ++s) mbar_init(mb0 + 8u * s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // rows t_begin+1 .. t_begin+NS-LAGMAX-1; the remaining slots are first
-    // armed by the per-step re-arm below (rows t-LAGMAX+NS for t >= t_begin)
 #pragma unroll
-    for (int k = 0; k < NS - G::LAGMAX - 1; ++k) issue(t_begin + 1 + k, k);
+    for (int k = 0; k < NS; ++k) issue(t_begin + 1 + k, k);
   }
   __syncwarp();
 
@@ -161,11 +156,11 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
     rhi[j] = min(ny, y1 - 1 + P.need[j][1]);
   }
 
-  double uu[NRR][NC];
+  double uu[NRR][NC], ff[NRR][NC];
 #pragma unroll
   for (int k = 0; k < NRR; ++k)
 #pragma unroll
-    for (int j = 0; j < NC; ++j) uu[k][j] = 0.0;
+    for (int j = 0; j < NC; ++j) uu[k][j] = ff[k][j] = 0.0;
 
   unsigned bad = 0;
   uint32_t round = 0;  // completed passes over the smem ring
@@ -182,9 +177,18 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
               mbar_wait(mb0 + 8u * SL, (round + (uint32_t)(KS / NS)) & 1u);
               const uint32_t a = ring + SL * G::SLOTB + lane * (NC * 8u);
 #pragma unroll
-              for (int k = 0; k < NP; ++k)
+              for (int k = 0; k < NP; ++k) {
                 asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
                              : "=d"(uu[RR][2 * k]), "=d"(uu[RR][2 * k + 1]) : "r"(a + 16u * k) : "memory");
+                if (FORM == 1)
+                  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                               : "=d"(ff[RR][2 * k]), "=d"(ff[RR][2 * k + 1]) : "r"(a + G::ROWB + 16u * k) : "memory");
+              }
+              __syncwarp();
+              if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(t + 1 + NS, SL);
+              }
             }
             // ---- phases in order ----
             [&]<int... Js>(std::integer_sequence<int, Js...>) {
@@ -235,12 +239,7 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                         if (FORM == 0) {
                           outv[k] = div_wc_used<DIV>(acc, valid[k], p);
                         } else {
-                          // f of row t-lag lives in ring slot (KS - lag - 1) mod NS
-                          constexpr int FS = ((KS - P.lag[J] - 1) % NS + NS) % NS;
-                          double fc;
-                          asm volatile("ld.shared.f64 %0, [%1];"
-                                       : "=d"(fc) : "r"(ring + FS * G::SLOTB + G::ROWB + lane * (NC * 8u) + 8u * cc) : "memory");
-                          const double qd = div_wc_used<DIV>(__dsub_rn(fc, acc), valid[k], p);
+                          const double qd = div_wc_used<DIV>(__dsub_rn(ff[R0][cc], acc), valid[k], p);
                           outv[k] = __dadd_rn(uc, __dmul_rn(p.omega, qd));
                         }
                       }
@@ -273,27 +272,14 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                 }
               }
             }
-            // row t-LAGMAX had its last phase: its slot takes row t-LAGMAX+NS
-            {
-              constexpr int SR = ((KS - G::LAGMAX - 1) % NS + NS) % NS;
-              __syncwarp();
-              if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(t - G::LAGMAX + NS, SR);
-              }
-            }
           }(),
           ...);
     }(std::make_integer_sequence<int, G::U>{});
   }
-  // drain: rows armed but never consumed must land before the CTA exits.
-  // After the last step tl-1 the armed rows are tl+1 .. tl-1-LAGMAX+NS.
+  // drain: the NS rows still in flight (one per slot) must land before exit
   if (lane == 0) {
-    const int t_last = t_begin + (int)round * G::U - 1;
-    for (int r = t_last + 2; r <= t_last - G::LAGMAX + NS; ++r) {
-      const int k = r - t_begin - 1;
-      mbar_wait(mb0 + 8u * (uint32_t)(k % NS), (uint32_t)((k / NS) & 1));
-    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) mbar_wait(mb0 + 8u * s, round & 1u);
   }
   __syncwarp();
   if (bad) atomicOr(p.status, 1);
