@@ -63,6 +63,9 @@ enum sl_form { SL_FORM_R = 0, SL_FORM_D = 1 };
                                       (reference _fault_merge_colours, strategies.py:364-369) */
 #define SL_FLAG_STREAM 0x4u        /* fused path: always the streaming kernels (no small-grid
                                       tile kernel, no on-chip patch kernel) — for testing */
+#define SL_FLAG_LEX 0x8u           /* lexicographic Gauss-Seidel order instead of colours: the
+                                      reference serial / taskgraph sweeps (strategies.py:341-345,
+                                      :477-487), run as hyperplane wavefronts */
 
 typedef struct sl_grid {
     int32_t dim;              /* 2 or 3 */

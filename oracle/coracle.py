@@ -44,8 +44,9 @@ def max_threads() -> int:
     return _load().oracle_max_threads()
 
 
-def sweep(u, name, sweeps=1, f=None, omega=0.8, form="R", threads=0):
-    """In-place colour sweeps of u (shape (..., S, S[, S]), C-contiguous fp64)."""
+def sweep(u, name, sweeps=1, f=None, omega=0.8, form="R", threads=0, order="colour"):
+    """In-place colour sweeps of u (shape (..., S, S[, S]), C-contiguous fp64).
+    order="lex": lexicographic (reference serial) sweeps instead."""
     dim, offsets, weights, wc, colours = STENCIL_TABLE[name]
     if not (u.flags.c_contiguous and u.dtype == np.float64):
         raise ValueError("u must be C-contiguous float64")
@@ -63,7 +64,8 @@ def sweep(u, name, sweeps=1, f=None, omega=0.8, form="R", threads=0):
             raise ValueError("form D needs f with u's shape")
         fp = f.ctypes.data
     rc = _load().oracle_sweep(dim, n, batch, grid, u.ctypes.data, fp, len(keep),
-                              off.ctypes.data, w.ctypes.data, wc, colours,
+                              off.ctypes.data, w.ctypes.data, wc,
+                              colours if order == "colour" else 0,
                               0 if form == "R" else 1, omega, sweeps, threads)
     if rc == 1:
         raise OracleNumericsError("non-finite update")

@@ -159,6 +159,40 @@ def sweep(u, name, sweeps=1, f=None, omega=None, form="R", origin=(0, 0, 0)):
     return u
 
 
+def lex_sweep(u, name, sweeps=1, f=None, omega=None, form="R"):
+    """Lexicographic Gauss-Seidel sweeps in place (reference serial sweep,
+    strategies.py:341-345: cells in increasing flat index, strategies.py:226-234,
+    each one kernels.py:224-232).  Pure-Python loops: small grids only."""
+    dim, offsets, weights, wc, _ = STENCIL_TABLE[name]
+    n = u.shape[-1] - 2
+    keep = [(off, w) for off, w in zip(offsets, weights) if w != 0.0]
+    flat = u.reshape(-1)
+    strides = [1, n + 2, (n + 2) ** 2][:dim]
+    deltas = [sum(o * s_ for o, s_ in zip(off, strides)) for off, _ in keep]
+    ws = [w for _, w in keep]
+    aws = [abs(w) for w in ws]
+    ff = f.reshape(-1) if f is not None else None
+    cells = sorted(sum((c + 1) * s_ for c, s_ in zip(coord, strides))
+                   for coord in np.ndindex(*((n,) * dim)))
+    for _ in range(sweeps):
+        for c in cells:
+            if form == "R":
+                acc = 0.0
+                for d, aw in zip(deltas, aws):
+                    acc = acc + aw * float(flat[c + d])
+                out = acc / wc
+            else:
+                uc = float(flat[c])
+                au = wc * uc
+                for d, w in zip(deltas, ws):
+                    au = au + w * float(flat[c + d])
+                out = uc + omega * ((float(ff[c]) - au) / wc)
+            if not np.isfinite(out):
+                raise OracleNumericsError("non-finite update")
+            flat[c] = out
+    return u
+
+
 def residual_max(u, name, f=None):
     """max |w_c u + sum_j w_j u_j| (kernels.py:254-265); with f: max |f - Au|."""
     dim, offsets, weights, wc, _ = STENCIL_TABLE[name]

@@ -40,6 +40,54 @@ typedef struct {
     int bad;
 } pass_args;
 
+/* one cell update in place; returns 1 when the new value is non-finite */
+static inline int update_point(double *ub, const double *fb, int64_t c, int form, int nnz,
+                               const int64_t *delta, const double *w, const double *aw,
+                               double wc, double omega)
+{
+    double out;
+    if (form == 0) {
+        double acc = 0.0;
+        for (int j = 0; j < nnz; ++j) {
+            double t = aw[j] * ub[c + delta[j]];
+            acc = acc + t;
+        }
+        out = acc / wc;
+    } else {
+        const double uc = ub[c];
+        double au = wc * uc;
+        for (int j = 0; j < nnz; ++j) {
+            double t = w[j] * ub[c + delta[j]];
+            au = au + t;
+        }
+        double q = (fb[c] - au) / wc;
+        double t = omega * q;
+        out = uc + t;
+    }
+    ub[c] = out;
+    return !isfinite(out);
+}
+
+/* Lexicographic Gauss-Seidel sweep (reference strategies.py:341-345 serial,
+ * cells in increasing flat index, strategies.py:226-234 / mesh.py:79-88). */
+static int lex_sweep(int dim, int64_t n, int64_t batch, int64_t bstride, double *u,
+                     const double *f, int nnz, const int64_t *delta, const double *w,
+                     const double *aw, double wc, int form, double omega)
+{
+    const int64_t S = n + 2;
+    int bad = 0;
+    for (int64_t b = 0; b < batch; ++b) {
+        double *ub = u + b * bstride;
+        const double *fb = f ? f + b * bstride : 0;
+        for (int64_t z = (dim == 3 ? 1 : 0); z < (dim == 3 ? n + 1 : 1); ++z)
+            for (int64_t y = 1; y <= n; ++y)
+                for (int64_t x = 1; x <= n; ++x)
+                    bad |= update_point(ub, fb, (z * S + y) * S + x, form, nnz, delta, w, aw,
+                                        wc, omega);
+    }
+    return bad;
+}
+
 static void *pass_rows(void *vp)
 {
     pass_args *a = (pass_args *)vp;
@@ -64,30 +112,9 @@ static void *pass_rows(void *vp)
         double *ub = a->u + b * a->bstride;
         const double *fb = a->f ? a->f + b * a->bstride : 0;
         const int64_t rowbase = (dim == 3) ? (z * S + y) * S : y * S;
-        for (int64_t x = 1 + qx; x <= n; x += 2) {
-            const int64_t c = rowbase + x;
-            double out;
-            if (a->form == 0) {
-                double acc = 0.0;
-                for (int j = 0; j < nnz; ++j) {
-                    double t = a->aw[j] * ub[c + a->delta[j]];
-                    acc = acc + t;
-                }
-                out = acc / a->wc;
-            } else {
-                const double uc = ub[c];
-                double au = a->wc * uc;
-                for (int j = 0; j < nnz; ++j) {
-                    double t = a->w[j] * ub[c + a->delta[j]];
-                    au = au + t;
-                }
-                double q = (fb[c] - au) / a->wc;
-                double t = a->omega * q;
-                out = uc + t;
-            }
-            if (!isfinite(out)) bad = 1;
-            ub[c] = out;
-        }
+        for (int64_t x = 1 + qx; x <= n; x += 2)
+            bad |= update_point(ub, fb, rowbase + x, a->form, nnz, a->delta, a->w, a->aw,
+                                a->wc, a->omega);
     }
     a->bad = bad;
     return 0;
@@ -129,6 +156,7 @@ static int colour_pass(int dim, int64_t n, int64_t batch, int64_t bstride,
  * off: nnz x 3 int32 displacements (x, y, z), canonical order, zero weights
  * already removed by the caller.  batch grids of (n+2)^dim, bstride apart.
  * form 0 = R (f ignored), 1 = D.  threads <= 0: all online cores.
+ * colours 0: lexicographic (serial) sweeps instead of colour passes.
  * Returns 0 ok, 1 non-finite update seen, 2 bad arguments.
  */
 int oracle_sweep(int dim, int64_t n, int64_t batch, int64_t bstride,
@@ -137,7 +165,7 @@ int oracle_sweep(int dim, int64_t n, int64_t batch, int64_t bstride,
                  double omega, int sweeps, int threads)
 {
     if ((dim != 2 && dim != 3) || n < 1 || nnz < 0 || nnz > MAXNB) return 2;
-    if (colours != 2 && colours != (1 << dim)) return 2;
+    if (colours != 0 && colours != 2 && colours != (1 << dim)) return 2;
     if (form == 1 && !f) return 2;
     if (threads <= 0) threads = oracle_max_threads();
     if (threads > MAXT) threads = MAXT;
@@ -148,6 +176,11 @@ int oracle_sweep(int dim, int64_t n, int64_t batch, int64_t bstride,
     double aw[MAXNB];
     for (int j = 0; j < nnz; ++j) aw[j] = fabs(w[j]);
     int bad = 0;
+    if (colours == 0) {
+        for (int s = 0; s < sweeps; ++s)
+            bad |= lex_sweep(dim, n, batch, bstride, u, f, nnz, delta, w, aw, wc, form, omega);
+        return bad;
+    }
     for (int s = 0; s < sweeps; ++s)
         for (int c = 0; c < colours; ++c)
             bad |= colour_pass(dim, n, batch, bstride, u, f, nnz, delta, w, aw, wc,

@@ -19,6 +19,7 @@ SL_FORM_R, SL_FORM_D = 0, 1
 SL_FLAG_PER_COLOUR = 0x1
 SL_FLAG_MERGE_COLOURS = 0x2
 SL_FLAG_STREAM = 0x4
+SL_FLAG_LEX = 0x8
 ABI_VERSION = 1
 
 # every symbol include/stencil_sweep.h declares (checked by tests/test_abi.py)

@@ -208,6 +208,15 @@ int sl_sweep(const sl_grid *g, const sl_stencil *s, int32_t sweeps, uint32_t fla
   if (!d_status || sweeps < 0) return SL_E_INVAL;
   if (sweeps == 0 || empty_grid(p)) return SL_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (flags & SL_FLAG_LEX) {
+    // lexicographic order is global: slabs (non-zero origin) are not supported
+    if (g->origin[0] || g->origin[1] || (g->dim == 3 && g->origin[2])) return SL_E_UNSUPPORTED;
+    for (int i = 0; i < sweeps; ++i) {
+      rc = cuda_status(launch_lex_sweep(key, p, st));
+      if (rc != SL_OK) return rc;
+    }
+    return SL_OK;
+  }
   if (flags & SL_FLAG_MERGE_COLOURS) {
     for (int i = 0; i < sweeps; ++i) {
       rc = cuda_status(launch_colour_pass(key, p, -1, st));

@@ -107,6 +107,43 @@ k1_residual(Params p, RowMap rm, unsigned long long *out) {
   if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
 }
 
+// Lexicographic Gauss-Seidel (reference serial sweep, strategies.py:341-345):
+// a point's earlier-in-lex neighbours all lie on smaller hyperplanes
+// t = x + y (+ z) (face stencils) or t = x + 2y (+ 4z) (box stencils) and its
+// later ones on larger hyperplanes, so sweeping the hyperplanes in order with
+// all points of one hyperplane in parallel reproduces the lex order exactly.
+template <int S, int FORM, bool UNIT, int DIV>
+__global__ void __launch_bounds__(256)
+k1_hyperplane(Params p, int64_t h, int64_t rows) {
+  constexpr int DIM = shape_dim(S);
+  constexpr int NNZ = shape_nnz(S);
+  constexpr bool FACE = (S == FD5 || S == FD7);
+  const int64_t ay = FACE ? 1 : 2, az = FACE ? 1 : 4;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t per_b = p.ny * p.nz;
+    const int64_t b = r / per_b;
+    const int64_t rem = r - b * per_b;
+    const int64_t z = DIM == 3 ? 1 + rem / p.ny : 0;
+    const int64_t y = 1 + rem % p.ny;
+    const int64_t x = h - ay * y - (DIM == 3 ? az * z : 0);
+    if (x < 1 || x > p.nx) continue;
+    double *ub = p.u + b * p.bstride;
+    const double *fb = FORM == 1 ? p.f + b * p.bstride : nullptr;
+    const int64_t c = z * p.sz + y * p.sy + x;
+    const double uc = ub[c];
+    double acc = acc_init<FORM, UNIT>(uc, p);
+#pragma unroll
+    for (int j = 0; j < NNZ; ++j) {
+      const Off o = shape_off(S, j);
+      acc = acc_add<FORM, UNIT>(acc, ub[c + o.x + o.y * p.sy + o.z * p.sz], j, p);
+    }
+    const double out = acc_finish<FORM, UNIT, DIV>(acc, uc, FORM == 1 ? fb[c] : 0.0, p);
+    if (!finite64(out)) atomicOr(p.status, 1);
+    ub[c] = out;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 
@@ -144,6 +181,27 @@ cudaError_t launch_colour_pass(const KernelKey &key, const Params &p, int colour
     note_launch();
     return cudaGetLastError();
   });
+}
+
+cudaError_t launch_lex_sweep(const KernelKey &key, const Params &p, cudaStream_t st) {
+  const int dim = shape_dim(key.shape);
+  const bool face = key.shape == FD5 || key.shape == FD7;
+  const int64_t ay = face ? 1 : 2, az = face ? 1 : 4;
+  const int64_t hmin = 1 + ay + (dim == 3 ? az : 0);
+  const int64_t hmax = p.nx + ay * p.ny + (dim == 3 ? az * p.nz : 0);
+  const int64_t rows = p.batch * p.ny * p.nz;
+  const int threads = 256;
+  int64_t blocks = (rows + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  cudaError_t e = cudaSuccess;
+  for (int64_t h = hmin; h <= hmax && e == cudaSuccess; ++h) {
+    e = dispatch(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
+      k1_hyperplane<S, F, U, D><<<(unsigned)blocks, threads, 0, st>>>(p, h, rows);
+      note_launch();
+      return cudaGetLastError();
+    });
+  }
+  return e;
 }
 
 cudaError_t launch_update_cells(const KernelKey &key, const Params &p, const int64_t *flats,

@@ -5,8 +5,11 @@ Covered strategies:
   hyb-sync    strategies.py:503-527 -> same result as colouring, bit for bit
   hyb-depend  strategies.py:490-500    (reference tests/test_strategies.py:142-152),
                                         so they run the same kernel
-Out of scope (lexicographic or thread-count-dependent update orders, not
-colour schedules): serial, nd, taskgraph — they raise NotImplementedError.
+  serial      strategies.py:341-345 -> lexicographic Gauss-Seidel as hyperplane
+  taskgraph   strategies.py:477-487    wavefronts (SL_FLAG_LEX); taskgraph equals
+                                        serial bit for bit (tests/test_strategies.py:125-139)
+Out of scope: nd (nested dissection) — its order depends on the CPU worker
+count; it raises NotImplementedError.
 
 Colour classes are parity relative to cell (1,..,1) (strategies.py:62-69):
 face stencils 2-colour on coordinate-sum parity, full neighbourhoods use the
@@ -30,7 +33,7 @@ __all__ = ["STRATEGY_IDS", "GPU_STRATEGIES", "canonical_strategy", "colour_count
            "run_sweep", "run_sweeps"]
 
 STRATEGY_IDS = ("serial", "colouring", "nd", "taskgraph", "hyb-depend", "hyb-sync")
-GPU_STRATEGIES = ("colouring", "hyb-depend", "hyb-sync")
+GPU_STRATEGIES = ("serial", "colouring", "taskgraph", "hyb-depend", "hyb-sync")
 
 _ALIASES = {
     "nested_dissection": "nd",
@@ -171,12 +174,16 @@ def sweep_hyb_depend(pool, mesh, kind, cost, chunk=1, plan=None):
 
 def _out_of_scope(name):
     raise NotImplementedError(
-        f"strategy {name!r} is not a colour schedule (lexicographic / thread-dependent order); "
-        "only colouring, hyb-sync and hyb-depend run on the GPU")
+        f"strategy {name!r} has a CPU-worker-count-dependent update order; "
+        f"the GPU runs {GPU_STRATEGIES}")
 
 
 def sweep_serial(mesh, kind, cost, plan=None, log=None):
-    _out_of_scope("serial")
+    """Lexicographic Gauss-Seidel sweep (reference strategies.py:341-345), on
+    the GPU as hyperplane wavefronts; bitwise equal to the reference."""
+    if log is not None:
+        raise NotImplementedError("per-cell tracing is not available on the GPU path")
+    run_sweeps(mesh, kind, cost, 1, plan=plan, flags=_native.SL_FLAG_LEX)
 
 
 def sweep_nested_dissection(pool, mesh, kind, cost, plan=None):
@@ -184,7 +191,9 @@ def sweep_nested_dissection(pool, mesh, kind, cost, plan=None):
 
 
 def sweep_taskgraph(pool, mesh, kind, cost, chunk=1, plan=None):
-    _out_of_scope("taskgraph")
+    """Dependence-DAG sweep; equals the serial sweep bit for bit (reference
+    tests/test_strategies.py:125-139), so it runs the lexicographic wavefront."""
+    run_sweeps(mesh, kind, cost, 1, plan=plan, flags=_native.SL_FLAG_LEX)
 
 
 def run_sweep(strategy: str, mesh: Mesh, kind: StencilKind, cost: CostModel,

@@ -252,3 +252,63 @@ def test_host_edits_between_sweeps_are_seen():
     m.values.fill(2.0)
     sl.run_sweeps(m, sl.FD5, sl.CostModel(), 1)
     assert (m.values == 2.0).all()
+
+
+# -- lexicographic order (serial / taskgraph) ---------------------------------
+
+@pytest.mark.parametrize("strategy", ["serial", "taskgraph"])
+def test_lex_matches_reference_serial_digests(ref_digests, strategy):
+    """Reference serial == taskgraph (strategies.py:341-345, :477-487)."""
+    for key, want in ref_digests["serial"].items():
+        name, n, sweeps, seed, b = _parse(key)
+        kind = sl.get_stencil(name)
+        with sl.StrategyRunner(kind.dim, n, kind, sl.CostModel(), strategy, threads=3,
+                               seed=seed, boundary=b) as r:
+            r.reinit()
+            r.run_sweeps(sweeps)
+            assert r.digest() == want, (key, strategy)
+
+
+def test_lex_small_buffers_bitwise():
+    small = np.load(os.path.join(GOLDEN, "reference_small.npz"))
+    for name in ("fd5", "fe9", "fd7", "fe27"):
+        kind = sl.get_stencil(name)
+        m = sl.make_mesh(kind.dim, 10 if kind.dim == 2 else 6, seed=11)
+        for _ in range(5):
+            sl.sweep_serial(m, kind, sl.CostModel())
+        assert _bits_equal(m.values, small["serial_" + name]), name
+
+
+def test_lex_kat_degenerate_row():
+    """Restates reference tests/test_strategies.py:74-89 on the device."""
+    a, b, c = 0.8, 0.3, 0.5
+    m = sl.Mesh(2, 3)
+    for x, v in ((1, a), (2, b), (3, c)):
+        m.values[m.flat_index((x, 1))] = v
+    sl.sweep_serial(m, sl.FD5, sl.CostModel())
+    a2 = b / 4
+    b2 = (a2 + c) / 4
+    got = [m.values[m.flat_index((x, 1))] for x in (1, 2, 3)]
+    assert got == [a2, b2, b2 / 4]
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_lex_form_d_matches_oracle_ragged(name):
+    dim = R.STENCIL_TABLE[name][0]
+    kind = sl.get_stencil(name)
+    for n in ((1, 2, 5, 16, 67) if dim == 2 else (1, 2, 5, 12)):
+        u = R.init_u(dim, n, n)
+        f = R.init_f(dim, n, n + 1)
+        coracle.sweep(u, name, 3, f=f, omega=0.8, form="D", order="lex")
+        m = sl.make_mesh(dim, n, seed=n)
+        sl.init_rhs(m, n + 1, 0.8)
+        sl.run_sweeps(m, kind, sl.CostModel(), 3, flags=_native.SL_FLAG_LEX)
+        assert _bits_equal(m.values, u), (name, n)
+
+
+def test_lex_differs_from_colour_order():
+    m1 = sl.make_mesh(2, 16, seed=1)
+    m2 = sl.make_mesh(2, 16, seed=1)
+    sl.sweep_serial(m1, sl.FD5, sl.CostModel())
+    sl.run_sweeps(m2, sl.FD5, sl.CostModel(), 1)
+    assert not _bits_equal(m1.values, m2.values)

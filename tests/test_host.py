@@ -90,9 +90,8 @@ def test_dispatch_errors_follow_reference():
         sl.run_sweep("bogus", m, sl.FD5, sl.CostModel())
     with pytest.raises(ValueError):
         sl.run_sweep("colouring", m, sl.FD5, sl.CostModel(), pool=None)
-    for strat in ("serial", "nd", "taskgraph"):
-        with pytest.raises(NotImplementedError):
-            sl.run_sweep(strat, m, sl.FD5, sl.CostModel(), pool=sl.DevicePool())
+    with pytest.raises(NotImplementedError):
+        sl.run_sweep("nd", m, sl.FD5, sl.CostModel(), pool=sl.DevicePool())
     assert strategies.canonical_strategy("hyb_sync") == "hyb-sync"
     with pytest.raises(ValueError):
         sl.SweepPlan(sl.Mesh(3, 4), sl.FD5, sl.CostModel())
@@ -114,7 +113,7 @@ def test_stencil_kind_accepts_zero_weights_rejects_positive():
 def test_bench_config_validation():
     runner.BenchConfig(dim=2, stencil="fe9", strategy="hyb-sync").validated()
     for bad in (dict(dim=4), dict(stencil="nope"), dict(dim=3, stencil="fd5"),
-                dict(strategy="serial"), dict(sizes=(0,)), dict(sweeps=0), dict(reps=0)):
+                dict(strategy="nd"), dict(sizes=(0,)), dict(sweeps=0), dict(reps=0)):
         with pytest.raises(runner.ConfigError):
             runner.BenchConfig(**bad).validated()
     assert runner.parse_cost("const:7").k == 7

@@ -166,3 +166,52 @@ def test_nonfinite_raises():
         R.colour_pass(u, "fd5", 0)
     with pytest.raises(R.OracleNumericsError):
         coracle.sweep(u, "fd5", 1)
+
+
+# -- lexicographic (serial) order ---------------------------------------------
+
+@pytest.mark.parametrize("impl", ["numpy", "c"])
+def test_lex_matches_reference_serial_digests(ref_digests, impl):
+    """Reference serial == taskgraph digests (strategies.py:341-345, :477-487)."""
+    for key, want in ref_digests["serial"].items():
+        name, n, sweeps, seed, b = _parse(key)
+        u = R.init_u(R.STENCIL_TABLE[name][0], n, seed, b)
+        if impl == "numpy":
+            R.lex_sweep(u, name, sweeps)
+        else:
+            coracle.sweep(u, name, sweeps, order="lex")
+        assert _digest(u) == want, (key, impl)
+
+
+def test_lex_small_buffers_bitwise():
+    small = np.load(os.path.join(GOLDEN, "reference_small.npz"))
+    for name in REF_KINDS:
+        dim = R.STENCIL_TABLE[name][0]
+        u = R.init_u(dim, 10 if dim == 2 else 6, 11)
+        coracle.sweep(u, name, 5, order="lex")
+        assert np.array_equal(u.reshape(-1).view(np.int64),
+                              small["serial_" + name].view(np.int64)), name
+
+
+def test_lex_kat_degenerate_row():
+    """One live row (a, b, c) under a zero halo: a'=b/4, b'=(a'+c)/4, c'=b'/4
+    (restates reference tests/test_strategies.py:74-89)."""
+    a, b, c = 0.8, 0.3, 0.5
+    u = np.zeros((5, 5))
+    u[1, 1:4] = (a, b, c)
+    R.lex_sweep(u, "fd5", 1)
+    a2 = b / 4
+    b2 = (a2 + c) / 4
+    assert tuple(u[1, 1:4]) == (a2, b2, b2 / 4)
+
+
+@pytest.mark.parametrize("name", list(R.STENCIL_TABLE))
+def test_lex_numpy_and_c_agree_form_d(name):
+    dim = R.STENCIL_TABLE[name][0]
+    n = 11 if dim == 2 else 5
+    u = R.init_u(dim, n, 2)
+    f = R.init_f(dim, n, 3)
+    v = u.copy()
+    R.lex_sweep(u, name, 2, f=f, omega=0.8, form="D")
+    coracle.sweep(v, name, 2, f=f, omega=0.8, form="D", order="lex")
+    assert np.array_equal(u.view(np.int64), v.view(np.int64))
