@@ -117,6 +117,29 @@ SL_API int sl_colour_pass(const sl_grid *g, const sl_stencil *s, int32_t colour,
 SL_API int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats,
                     int64_t count, int32_t *d_status, void *stream);
 
+/* Cost model (reference kernels.py:113-145): k sine evaluations per stencil
+ * entry and centre, folded into the weights as 0.0*d so the values stay
+ * bit-identical to k = 0; the consumed sine sum is added to *d_work. */
+#define SL_COST_CONST 0
+#define SL_COST_RAMP 1 /* k = min(100*rank/total, 99), rank = lex rank of the cell in its grid */
+typedef struct sl_cost {
+    int32_t mode;   /* SL_COST_CONST / SL_COST_RAMP */
+    int32_t k;      /* SL_COST_CONST: k >= 0 */
+    double *d_work; /* device double accumulator for the sine tally, or NULL */
+} sl_cost;
+
+/* `sweeps` sweeps with the cost model: colour order by default, lexicographic
+ * with SL_FLAG_LEX (the only flag honoured).  One launch per colour phase /
+ * hyperplane; replaces the k > 0 paths of strategies.py:341-393.  Ramp cost
+ * needs origin 0 (the rank is lexicographic over the whole grid). */
+SL_API int sl_sweep_cost(const sl_grid *g, const sl_stencil *s, const sl_cost *cost,
+                         int32_t sweeps, uint32_t flags, int32_t *d_status, void *stream);
+
+/* update_cells_batch with k > 0 (kernels.py:234-244); mode must be CONST. */
+SL_API int sl_update_cells_cost(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats,
+                                int64_t count, const sl_cost *cost, int32_t *d_status,
+                                void *stream);
+
 /* Ghost depth along the slowest axis (z in 3D, y in 2D) needed to run
  * `sweeps` colour-ordered sweeps on a slab without exchanging: the input must
  * be valid this many planes beyond the slab for its own planes to come out

@@ -12,8 +12,9 @@ from .kernels import (FD5, FD7, FE9, FE27, FE27Q1, STENCILS, CostModel, Numerics
 from .mesh import Mesh, init, init_rhs, make_mesh
 from .patches import PatchBatch, init_patches
 from .pool import DevicePool, Schedule, WorkerPool
-from .runner import (BenchConfig, BenchResult, ConfigError, StrategyRunner, mesh_digest,
-                     parse_cost, run_benchmark)
+from .runner import (CONVERGENCE_TOL, BenchConfig, BenchResult, ConfigError, Report,
+                     StrategyRunner, mesh_digest, parse_cost, run_benchmark, run_verification,
+                     serial_convergence_budget, verify_convergence, verify_oracle)
 from .strategies import (GPU_STRATEGIES, STRATEGY_IDS, SweepPlan, colour_count, colour_of,
                          run_sweep, run_sweeps, sweep_colouring, sweep_colouring_reference,
                          sweep_hyb_depend, sweep_hyb_sync, sweep_nested_dissection, sweep_serial,

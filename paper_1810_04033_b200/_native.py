@@ -20,12 +20,14 @@ SL_FLAG_PER_COLOUR = 0x1
 SL_FLAG_MERGE_COLOURS = 0x2
 SL_FLAG_STREAM = 0x4
 SL_FLAG_LEX = 0x8
+SL_COST_CONST, SL_COST_RAMP = 0, 1
 ABI_VERSION = 1
 
 # every symbol include/stencil_sweep.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sl_abi_version", "sl_strerror", "sl_last_cuda_error", "sl_launch_count",
            "sl_workspace_bytes",
-           "sl_sweep", "sl_colour_pass", "sl_update_cells", "sl_residual_max", "sl_ghost_depth")
+           "sl_sweep", "sl_colour_pass", "sl_update_cells", "sl_residual_max", "sl_ghost_depth",
+           "sl_sweep_cost", "sl_update_cells_cost")
 
 
 class NativeLibraryError(RuntimeError):
@@ -46,6 +48,10 @@ class SlStencil(ctypes.Structure):
                 ("omega", ctypes.c_double)]
 
 
+class SlCost(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("k", ctypes.c_int32), ("d_work", ctypes.c_void_p)]
+
+
 _lib = None
 
 _P = ctypes.POINTER
@@ -64,6 +70,11 @@ _SIGS = {
     "sl_residual_max": (ctypes.c_int, [_P(SlGrid), _P(SlStencil), ctypes.c_void_p,
                                        ctypes.c_void_p]),
     "sl_ghost_depth": (ctypes.c_int, [_P(SlStencil), ctypes.c_int32, ctypes.c_int32]),
+    "sl_sweep_cost": (ctypes.c_int, [_P(SlGrid), _P(SlStencil), _P(SlCost), ctypes.c_int32,
+                                     ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p]),
+    "sl_update_cells_cost": (ctypes.c_int, [_P(SlGrid), _P(SlStencil), ctypes.c_void_p,
+                                            ctypes.c_int64, _P(SlCost), ctypes.c_void_p,
+                                            ctypes.c_void_p]),
 }
 
 

@@ -8,6 +8,7 @@
 
 #include "../../include/stencil_sweep.h"
 #include "k1_colour.cuh"
+#include "k5_cost.cuh"
 #include "k2_fused.cuh"
 #include "plan.cuh"
 
@@ -246,6 +247,46 @@ int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flat
   if (rc != SL_OK) return rc;
   if (!d_status || count < 0 || (count > 0 && !d_flats)) return SL_E_INVAL;
   return cuda_status(launch_update_cells(key, p, d_flats, count, (cudaStream_t)stream));
+}
+
+int sl_sweep_cost(const sl_grid *g, const sl_stencil *s, const sl_cost *cost, int32_t sweeps,
+                  uint32_t flags, int32_t *d_status, void *stream) {
+  KernelKey key;
+  Params p;
+  int rc = make_params(g, s, d_status, &key, &p);
+  if (rc != SL_OK) return rc;
+  if (!d_status || !cost || sweeps < 0 || (flags & ~SL_FLAG_LEX)) return SL_E_INVAL;
+  if (cost->mode != SL_COST_CONST && cost->mode != SL_COST_RAMP) return SL_E_INVAL;
+  if (cost->mode == SL_COST_CONST && cost->k < 0) return SL_E_INVAL;
+  const bool origin = g->origin[0] || g->origin[1] || (g->dim == 3 && g->origin[2]);
+  if (origin && (cost->mode == SL_COST_RAMP || (flags & SL_FLAG_LEX))) return SL_E_UNSUPPORTED;
+  if (sweeps == 0 || empty_grid(p)) return SL_OK;
+  CostSpec cs{cost->mode == SL_COST_RAMP, cost->k, cost->d_work};
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < sweeps; ++i) {
+    if (flags & SL_FLAG_LEX) {
+      rc = cuda_status(launch_cost_sweep_phase(key, p, cs, -1, st));
+      if (rc != SL_OK) return rc;
+      continue;
+    }
+    for (int c = 0; c < p.colours; ++c) {
+      rc = cuda_status(launch_cost_sweep_phase(key, p, cs, c, st));
+      if (rc != SL_OK) return rc;
+    }
+  }
+  return SL_OK;
+}
+
+int sl_update_cells_cost(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats,
+                         int64_t count, const sl_cost *cost, int32_t *d_status, void *stream) {
+  KernelKey key;
+  Params p;
+  int rc = make_params(g, s, d_status, &key, &p);
+  if (rc != SL_OK) return rc;
+  if (!d_status || !cost || count < 0 || (count > 0 && !d_flats)) return SL_E_INVAL;
+  if (cost->mode != SL_COST_CONST || cost->k < 0) return SL_E_INVAL;
+  CostSpec cs{0, cost->k, cost->d_work};
+  return cuda_status(launch_cost_cells(key, p, cs, d_flats, count, (cudaStream_t)stream));
 }
 
 int sl_ghost_depth(const sl_stencil *s, int32_t dim, int32_t sweeps) {

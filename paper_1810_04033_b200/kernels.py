@@ -151,9 +151,10 @@ def get_stencil(name: str) -> StencilKind:
 class CostModel:
     """Per-cell extra-work parameter k (reference kernels.py:113-145).
 
-    The GPU path implements k = 0 (every BASELINE config); k > 0 — inert
-    sine work that leaves the numbers unchanged — is the §8(f) "next" item and
-    raises NotImplementedError at sweep time.
+    k = 0 runs the fused bandwidth kernels; k > 0 (const or ramp) runs the
+    cost kernel (csrc/k5_cost.cu): k sine evaluations per stencil entry whose
+    sum is folded in as 0.0*d, so the values are bit-identical to k = 0 and
+    the consumed tally is returned by the sweep.
     """
 
     mode: str = "const"
@@ -180,10 +181,17 @@ class CostModel:
     def describe(self) -> str:
         return f"const:{self.k}" if self.mode == "const" else "ramp"
 
-    def require_gpu_supported(self):
-        if not (self.mode == "const" and self.k == 0):
-            raise NotImplementedError(
-                f"cost {self.describe()}: only k=0 runs on the GPU path (k>0 is a later item)")
+    @property
+    def is_free(self) -> bool:
+        """k = 0 everywhere: the bandwidth kernels apply."""
+        return self.mode == "const" and self.k == 0
+
+    def descriptor(self, d_work=None):
+        c = _native.SlCost()
+        c.mode = _native.SL_COST_CONST if self.mode == "const" else _native.SL_COST_RAMP
+        c.k = self.k if self.mode == "const" else 0
+        c.d_work = d_work
+        return c
 
 
 # ---------------------------------------------------------------------------
@@ -250,9 +258,8 @@ class ScalarCellKernel:
         self.work_sum = 0.0
 
     def update(self, nbrs, centre: int, k: int) -> float:
-        if k:
-            CostModel("const", k).require_gpu_supported()
-        update_cells_batch(self.mesh, self.kind, np.array([centre], dtype=np.int64), 0)
+        self.work_sum += update_cells_batch(self.mesh, self.kind,
+                                            np.array([centre], dtype=np.int64), k)
         return float(self.mesh.device_values()[centre].item())
 
 
@@ -266,21 +273,32 @@ def update_cell(mesh: Mesh, kind: StencilKind, coord, k: int = 0) -> float:
 
 def update_cells_batch(mesh: Mesh, kind: StencilKind, flats, k: int) -> float:
     """In-place update of mutually non-adjacent interior cells (reference
-    kernels.py:212-251) on the GPU; returns the (zero) work tally."""
-    if k:
-        CostModel("const", k).require_gpu_supported()
+    kernels.py:212-251) on the GPU; returns the consumed sine tally (0.0 when
+    k == 0)."""
+    if k < 0:
+        raise ValueError("k must be non-negative")
     call = _call(mesh, kind)
     import torch
     if isinstance(flats, torch.Tensor):
         d_flats = flats.to(device=call.status.device, dtype=torch.int64)
     else:
         d_flats = torch.from_numpy(np.ascontiguousarray(flats, dtype=np.int64)).to(call.status.device)
-    rc = _native.load().sl_update_cells(ctypes.byref(call.grid), ctypes.byref(call.stencil),
-                                        d_flats.data_ptr(), d_flats.numel(),
-                                        call.status.data_ptr(), call.stream)
+    lib = _native.load()
+    if k == 0:
+        rc = lib.sl_update_cells(ctypes.byref(call.grid), ctypes.byref(call.stencil),
+                                 d_flats.data_ptr(), d_flats.numel(),
+                                 call.status.data_ptr(), call.stream)
+        _native.check(rc, "update_cells_batch")
+        call.check_status("update_cells_batch")
+        return 0.0
+    work = torch.zeros(1, dtype=torch.float64, device=call.status.device)
+    cost = CostModel("const", k).descriptor(work.data_ptr())
+    rc = lib.sl_update_cells_cost(ctypes.byref(call.grid), ctypes.byref(call.stencil),
+                                  d_flats.data_ptr(), d_flats.numel(), ctypes.byref(cost),
+                                  call.status.data_ptr(), call.stream)
     _native.check(rc, "update_cells_batch")
     call.check_status("update_cells_batch")
-    return 0.0
+    return float(work.item())
 
 
 def residual_max(mesh: Mesh, kind: StencilKind) -> float:

@@ -79,17 +79,27 @@ class PatchBatch:
 
     def sweep(self, kind: StencilKind, sweeps: int = 1, cost: CostModel = CostModel(),
               flags: int = 0, check: bool = True):
-        """`sweeps` colour-ordered sweeps of every patch, in place."""
+        """`sweeps` colour-ordered sweeps of every patch, in place; returns the
+        cost-model sine tally (0.0 when k == 0)."""
         import torch
-        cost.require_gpu_supported()
         g, s = self._descriptors(kind)
         stream = torch.cuda.current_stream(self.u.device).cuda_stream
-        rc = _native.load().sl_sweep(ctypes.byref(g), ctypes.byref(s), sweeps, flags, None, 0,
-                                     self.status.data_ptr(), stream)
+        work = None
+        if cost.is_free:
+            rc = _native.load().sl_sweep(ctypes.byref(g), ctypes.byref(s), sweeps, flags, None, 0,
+                                         self.status.data_ptr(), stream)
+        else:
+            w = torch.zeros(1, dtype=torch.float64, device=self.u.device)
+            c = cost.descriptor(w.data_ptr())
+            rc = _native.load().sl_sweep_cost(ctypes.byref(g), ctypes.byref(s), ctypes.byref(c),
+                                              sweeps, flags & _native.SL_FLAG_LEX,
+                                              self.status.data_ptr(), stream)
+            work = w
         _native.check(rc, "patch sweep")
         if check and int(self.status.item()):
             self.status.zero_()
             raise NumericsError("non-finite update in a patch sweep")
+        return 0.0 if work is None else float(work.item())
 
 
 def init_patches(batch: int, n: int, seed: int):

@@ -124,12 +124,23 @@ def _plan_for(mesh, kind, cost, plan):
 
 
 def run_sweeps(mesh: Mesh, kind: StencilKind, cost: CostModel, sweeps: int,
-               plan: SweepPlan = None, flags: int = 0) -> None:
-    """`sweeps` colour-ordered sweeps in one library call (fused when possible)."""
-    cost.require_gpu_supported()
+               plan: SweepPlan = None, flags: int = 0) -> float:
+    """`sweeps` colour-ordered (or, with SL_FLAG_LEX, lexicographic) sweeps in
+    one library call (fused when possible); returns the consumed cost-model
+    sine tally (0.0 when k == 0)."""
     plan = _plan_for(mesh, kind, cost, plan)
     call = plan.device_call()
     lib = _native.load()
+    if not cost.is_free:
+        import torch
+        work = torch.zeros(1, dtype=torch.float64, device=call.status.device)
+        desc = cost.descriptor(work.data_ptr())
+        rc = lib.sl_sweep_cost(ctypes.byref(call.grid), ctypes.byref(call.stencil),
+                               ctypes.byref(desc), sweeps, flags & _native.SL_FLAG_LEX,
+                               call.status.data_ptr(), call.stream)
+        _native.check(rc, "sweep")
+        call.check_status("sweep")
+        return float(work.item())
     ws_bytes = 0
     ws_ptr = None
     if not flags:
@@ -140,6 +151,7 @@ def run_sweeps(mesh: Mesh, kind: StencilKind, cost: CostModel, sweeps: int,
                       ws_ptr, ws_bytes, call.status.data_ptr(), call.stream)
     _native.check(rc, "sweep")
     call.check_status("sweep")
+    return 0.0
 
 
 def sweep_colouring(pool: DevicePool, mesh: Mesh, kind: StencilKind, cost: CostModel,

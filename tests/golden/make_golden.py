@@ -19,6 +19,7 @@ writes:
                            "serial_<kind>" = the same after 5 lexicographic sweeps
   reference_digests.json["serial"]  sha256 after serial sweeps (strategies.py:341-345),
                            checked equal to taskgraph here (tests/test_strategies.py:125-139)
+  reference_digests.json["convergence"]  serial_convergence_budget (bench.py:433-442)
 
 The GPU box never reads /root/reference: tests compare against these files.
 """
@@ -32,7 +33,7 @@ import numpy as np
 
 sys.path.insert(0, "/root/reference/pkg/src")
 
-from stencil_lab.bench import StrategyRunner, mesh_digest  # noqa: E402
+from stencil_lab.bench import StrategyRunner, mesh_digest, serial_convergence_budget  # noqa: E402
 from stencil_lab.kernels import STENCILS, CostModel, residual_max  # noqa: E402
 from stencil_lab.mesh import Mesh, init, make_mesh  # noqa: E402
 from stencil_lab.strategies import sweep_colouring_reference, sweep_serial  # noqa: E402
@@ -41,7 +42,11 @@ OUT = os.path.dirname(os.path.abspath(__file__))
 
 
 def main():
-    digests = {"sweeps": {}, "init": {}, "residual": {}, "serial": {}}
+    digests = {"sweeps": {}, "init": {}, "residual": {}, "serial": {}, "convergence": {}}
+    # serial sweep counts to residual < 1e-8 (bench.py:433-442), criterion-6 cases
+    for name, n in (("fd5", 33), ("fd7", 17), ("fe9", 17), ("fe27", 9)):
+        digests["convergence"][f"{name}/n={n}/seed=7"] = serial_convergence_budget(
+            STENCILS[name], n, seed=7)
     # criterion-5 style: all kinds, n in {8, 33}, 100 sweeps, seed 42
     for name, kind in STENCILS.items():
         for n in (8, 33):

@@ -50,13 +50,15 @@ def test_struct_layout_matches_header(tmp_path):
         '#include <stdio.h>\n#include <stddef.h>\n#include "stencil_sweep.h"\n'
         'int main(void){printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(sl_grid), offsetof(sl_grid,u),'
         ' offsetof(sl_grid,f), sizeof(sl_stencil), offsetof(sl_stencil,w), offsetof(sl_stencil,wc),'
-        ' offsetof(sl_stencil,omega));return 0;}\n')
+        ' offsetof(sl_stencil,omega));printf("%zu %zu %zu\\n", sizeof(sl_cost), offsetof(sl_cost,k),'
+        ' offsetof(sl_cost,d_work));return 0;}\n')
     exe = tmp_path / "layout"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(prog)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     want = [ctypes.sizeof(_native.SlGrid), _native.SlGrid.u.offset, _native.SlGrid.f.offset,
             ctypes.sizeof(_native.SlStencil), _native.SlStencil.w.offset,
-            _native.SlStencil.wc.offset, _native.SlStencil.omega.offset]
+            _native.SlStencil.wc.offset, _native.SlStencil.omega.offset,
+            ctypes.sizeof(_native.SlCost), _native.SlCost.k.offset, _native.SlCost.d_work.offset]
     assert got == want
 
 
@@ -94,6 +96,27 @@ def test_invalid_arguments_rejected_before_launch():
     g.batch = 2
     g.batch_stride = 10                                           # overlapping grids
     assert _sweep(g, s) == _native.SL_E_INVAL
+
+
+def test_cost_sweep_arguments_rejected_before_launch():
+    lib = _native.load()
+    s = FD5.descriptor(_native.SL_FORM_R)
+
+    def call(cost, flags=0, g=None):
+        return lib.sl_sweep_cost(ctypes.byref(g or _grid()), ctypes.byref(s),
+                                 ctypes.byref(cost), 1, flags, 0x2000, None)
+
+    bad_mode = _native.SlCost(7, 1, None)
+    assert call(bad_mode) == _native.SL_E_INVAL
+    assert call(_native.SlCost(_native.SL_COST_CONST, -1, None)) == _native.SL_E_INVAL
+    assert call(_native.SlCost(_native.SL_COST_CONST, 1, None),
+                flags=_native.SL_FLAG_STREAM) == _native.SL_E_INVAL
+    g = _grid()
+    g.origin[1] = 5                                               # slab: ramp rank is global
+    assert call(_native.SlCost(_native.SL_COST_RAMP, 0, None), g=g) == _native.SL_E_UNSUPPORTED
+    assert lib.sl_update_cells_cost(ctypes.byref(_grid()), ctypes.byref(s), None, 1,
+                                    ctypes.byref(_native.SlCost(_native.SL_COST_CONST, 2, None)),
+                                    0x2000, None) == _native.SL_E_INVAL
 
 
 def test_zero_sweeps_and_empty_grid_are_noops():

@@ -10,7 +10,7 @@ import pytest
 
 import paper_1810_04033_b200 as sl
 from oracle import restate as R
-from paper_1810_04033_b200 import runner, strategies
+from paper_1810_04033_b200 import _native, runner, strategies
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -97,11 +97,15 @@ def test_dispatch_errors_follow_reference():
         sl.SweepPlan(sl.Mesh(3, 4), sl.FD5, sl.CostModel())
 
 
-def test_cost_k_positive_not_on_gpu_path():
-    with pytest.raises(NotImplementedError):
-        sl.CostModel("const", 3).require_gpu_supported()
-    sl.CostModel("const", 0).require_gpu_supported()
+def test_cost_model_descriptor():
+    assert sl.CostModel("const", 0).is_free
+    assert not sl.CostModel("const", 3).is_free and not sl.CostModel("ramp").is_free
+    d = sl.CostModel("const", 3).descriptor()
+    assert (d.mode, d.k) == (_native.SL_COST_CONST, 3)
+    assert sl.CostModel("ramp").descriptor().mode == _native.SL_COST_RAMP
     assert sl.CostModel("ramp").k_for_rank(99, 100) == 99
+    with pytest.raises(ValueError):
+        sl.CostModel("const", -1)
 
 
 def test_stencil_kind_accepts_zero_weights_rejects_positive():
@@ -128,6 +132,23 @@ def test_csv_round_trip():
     assert rows[0] == runner.CSV_HEADER
     back = runner.parse_csv("\n".join(rows))
     assert back[0].seconds == [0.5, 0.25] and back[0].digests == ["a", "a"]
+    assert rows[1].endswith(",a,,1") and back[0].gpus == 1
+    # reference-layout CSV (no device columns) still parses
+    ref = [runner.REFERENCE_CSV_HEADER] + [",".join(row.split(",")[:13]) for row in rows[1:]]
+    back = runner.parse_csv(ref)
+    assert back[0].seconds == [0.5, 0.25]
+    with pytest.raises(ValueError):
+        runner.parse_csv([runner.CSV_HEADER, "1,2,3"])
+
+
+def test_cli_configuration_errors_exit_2(capsys):
+    from paper_1810_04033_b200 import cli
+    assert cli.main(["run", "--dim", "3", "--stencil", "fd5"]) == 2
+    assert cli.main(["run", "--cost", "linear"]) == 2
+    assert cli.main(["run", "--strategy", "nd"]) == 2
+    assert cli.main(["trace"]) == 2
+    assert cli.main(["verify", "--suite", "races"]) == 2
+    assert "configuration error" in capsys.readouterr().err
 
 
 def test_schedule_parse():

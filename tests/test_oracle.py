@@ -215,3 +215,18 @@ def test_lex_numpy_and_c_agree_form_d(name):
     R.lex_sweep(u, name, 2, f=f, omega=0.8, form="D")
     coracle.sweep(v, name, 2, f=f, omega=0.8, form="D", order="lex")
     assert np.array_equal(u.view(np.int64), v.view(np.int64))
+
+
+def test_lex_convergence_budget_matches_reference(ref_digests):
+    """serial_convergence_budget (bench.py:433-442) replayed on the C lex sweep."""
+    for key, want in ref_digests["convergence"].items():
+        name = key.split("/")[0]
+        n = int(key.split("n=")[1].split("/")[0])
+        u = R.init_u(R.STENCIL_TABLE[name][0], n, 7)
+        got = None
+        for s in range(1, 20001):
+            coracle.sweep(u, name, 1, order="lex", threads=1)
+            if R.residual_max(u, name) < 1e-8:
+                got = s
+                break
+        assert got == want, key
