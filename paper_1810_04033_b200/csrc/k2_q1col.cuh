@@ -9,40 +9,60 @@
 //
 // A CTA owns a 64 x 32 (x, y) tile (+ the ghost margin 4/4/2 of the plan) and
 // a chunk of z.  Thread (warp w, lane i) owns column pair (2i, 2i+1) of the
-// two tile rows r0 = 2w + delta, r0 + 1, where delta makes row r0 the y-parity
-// 0 row: a colour group updates all columns of every other row, so each
-// thread updates both points of one of its rows per group.  The thread keeps
-// its two rows of the pair for planes t-6 .. t+1 in a register ring (z and
-// own-row neighbours), gets the neighbour pair's columns by warp shuffles,
-// and reads only the rows owned by the warps above/below from shared memory.
-// Updated pairs are written back to the plane's smem slot for those readers.
-// u planes arrive by TMA (64 x 33 x 1 boxes, zero-filled out of range) into 9
-// smem slots, D = 2 planes ahead; f is prefetched one step ahead per thread.
+// RT = 4 tile rows r0 = 4w + delta .. r0 + 3, where delta makes row r0 a
+// y-parity 0 row: a colour group updates all columns of every other row, so
+// each thread updates 2 x 2 points (rows A, A + 2) per group.  The thread
+// keeps its rows for the R = 8 most recent planes in a register ring (255
+// registers per thread at 256 threads), reads the row owned by the warp
+// above/below from the plane's shared-memory slot, and gets the x+-1 columns
+// by warp shuffles.  Updated pairs are published back to the slot (after both
+// groups of the step have read their inputs) for the warps above/below.
+//
+// u planes arrive by TMA (64 x 33 x 1 boxes, zero-filled out of range) into
+// R = 8 smem slots, issued two planes ahead; plane P lives in slot and ring
+// entry (P - base) mod 8 and the step loop is unrolled by 8, so every slot
+// offset, ring index and mbarrier parity is a compile-time constant.
+// Out-of-range groups and ghost points are computed and masked (no branches
+// around the shuffles); the exact-division fallback is taken per warp only
+// when some used lane's operand is outside the fast range.
 #pragma once
 #include <cuda.h>
 
 #include "plan.cuh"
 
+#ifndef Q1_ROWS_PER_THREAD
+#define Q1_ROWS_PER_THREAD 4
+#endif
+
 namespace sl {
 
-struct Q1Geo {
+// Exact division out of line: the rare fallback of the Markstein fast path
+// must not bloat the unrolled step loop (instruction-cache pressure).
+__device__ __noinline__ double q1_div_exact(double a, double b) { return __ddiv_rn(a, b); }
+
+template <int RT_>
+struct Q1GeoT {
   static constexpr FPlan P = make_plan(Q1, 8, 1, true);
   static constexpr int LAGMAX = P.lagmax;                 // 4
   static constexpr int GX = 4, GY = 4, GZ = 2;            // plan load margins
   static constexpr int PX = 64, PY = 32;                  // tile incl. ghost
   static constexpr int BOXY = PY + 1;                     // rows loaded (delta shift)
   static constexpr int TX = PX - 2 * GX, TY = PY - 2 * GY;
-  static constexpr int RR = 8;                            // register ring (planes t-6 .. t+1)
-  static constexpr int WS = 9;                            // smem slots (planes t-5 .. t+3)
-  static constexpr int D = 2;                             // TMA lookahead beyond plane t+1
-  static constexpr int NT = 512;
+  static constexpr int R = 8;                             // ring = smem slots = unroll
+  static constexpr int RR = R;
+  static constexpr int RT = RT_;                          // tile rows per thread
+  static constexpr int NT = 32 * PY / RT;
   static constexpr int SLOTE = PX * BOXY;
   static constexpr int LEADE = 2 * PX;                    // guard rows before slot 0
-  static constexpr size_t SMEM = size_t(LEADE + WS * SLOTE + 2 * PX) * sizeof(double) + WS * 8;
+  static constexpr size_t SMEM = size_t(LEADE + R * SLOTE + 2 * PX) * sizeof(double) + R * 8;
   static_assert(P.lag[0] == 0 && P.lag[2] == 1 && P.lag[4] == 3 && P.lag[6] == 4, "unexpected plan");
+  static_assert(P.lag[1] == P.lag[0] && P.lag[3] == P.lag[2] && P.lag[5] == P.lag[4] &&
+                    P.lag[7] == P.lag[6], "colour pairs share a lag");
   static_assert(P.load[0] <= GX && P.load[1] <= GY && P.load[2] <= GZ, "ghost margin");
-  static_assert(WS >= LAGMAX + 3 + D && RR >= LAGMAX + 3, "rings too short");
+  // planes t-5 .. t+1 are read at step t and plane t+2 is in flight
+  static_assert(R >= LAGMAX + 4, "ring too short");
 };
+using Q1Geo = Q1GeoT<Q1_ROWS_PER_THREAD>;
 
 template <int FORM, bool UNIT, int DIV>
 __global__ void __launch_bounds__(Q1Geo::NT, 1)
@@ -50,10 +70,10 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
          int64_t nty, int64_t nzc) {
   using G = Q1Geo;
   constexpr FPlan P = G::P;
-  constexpr int RR = G::RR, WS = G::WS, D = G::D;
+  constexpr int R = G::R;
   extern __shared__ __align__(128) double qsm[];
   double *su = qsm + G::LEADE;  // slot k at su + k*SLOTE
-  uint64_t *mb = reinterpret_cast<uint64_t *>(su + WS * G::SLOTE + 2 * G::PX);
+  uint64_t *mb = reinterpret_cast<uint64_t *>(su + R * G::SLOTE + 2 * G::PX);
   const uint32_t su_s = (uint32_t)__cvta_generic_to_shared(su);
   const uint32_t mb_s = (uint32_t)__cvta_generic_to_shared(mb);
 
@@ -69,219 +89,275 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gx = gx0 + 2 * lane;
   const int delta = (1 - p.py - gy0) & 1;        // local row r0 has y parity 0
-  const int r0 = 2 * warp + delta;               // this thread's rows: r0 (qy 0), r0 + 1 (qy 1)
-  const int sy = (int)p.sy;
+  const int r0 = G::RT * warp + delta;           // this thread's rows r0 (qy 0) .. r0 + RT - 1
   const int64_t sz = p.sz;
 
   int t_begin = z0 - G::GZ - 1;
   if ((t_begin - 1 + p.pz) & 1) --t_begin;       // plane parity of step k is k & 1
   const int t_end = z1 - 1 + G::LAGMAX;
   const int zlim = z1 + G::GZ;
-
-  // smem slot offsets (elements), rotated per step: so[k] = slot of plane t+1+D-k
-  int so[WS];
-#pragma unroll
-  for (int k = 0; k < WS; ++k) so[k] = (((t_begin + 1 + D - k) % WS + WS) % WS) * G::SLOTE;
+  const int base = t_begin + 1;                  // plane held by slot 0 in use 0
 
   auto issue = [&](int plane) {
-    const int sl = ((plane % WS) + WS) % WS;
+    const int sl = (plane - base) & (R - 1);
     const uint32_t bar = mb_s + 8u * sl;
     const bool live = plane >= 0 && plane < Sz && plane < zlim;
     mbar_expect3(bar, live ? (uint32_t)(G::SLOTE * 8) : 0u);
     if (live) tma_load_3d(su_s + sl * G::SLOTE * 8, &tmu, gx0, gy0, plane, bar);
   };
-  // use count of the slot holding `plane` (planes >= t_begin+1 are loaded, in order)
-  auto parity_of = [&](int plane) -> uint32_t {
-    const int sl = ((plane % WS) + WS) % WS;
-    const int first = t_begin + 1 + (((sl - (t_begin + 1)) % WS) + WS) % WS;  // first plane in slot
-    return (uint32_t)(((plane - first) / WS) & 1);
-  };
 
   if (threadIdx.x == 0) {
-    for (int k = 0; k < WS; ++k) mbar_init3(mb_s + 8u * k);
+    for (int k = 0; k < R; ++k) mbar_init3(mb_s + 8u * k);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int k = 1; k <= 1 + D; ++k) issue(t_begin + k);
+    issue(base);
+    issue(base + 1);
   }
   __syncthreads();
 
-  // validity per group (need margins are per colour group; both colours of a
-  // group share them): group g = J/2 for J = 0,2,4,6
-  auto colok = [&](int s, int need) -> bool {
-    const int lx = 2 * lane + s;
-    return lx >= G::GX - need && lx < G::GX + TXo + need && gx + s >= 1 && gx + s <= nx;
-  };
-  auto rowok = [&](int r, int need) -> bool {
-    const int gy = gy0 + r;
-    return r >= G::GY - need && r < G::GY + TYo + need && gy >= 1 && gy <= ny;
-  };
-
-  double U[2][RR][2];   // [row][plane ring][col]
+  // ---- thread-constant masks ------------------------------------------------
+  // ok bit (4*gi + 2*h + s): point s of the h-th row (A + 2h) of group gi
+  // (J = 2*gi) is inside the group's need region and the grid interior (x, y)
+  unsigned okbits = 0;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int gi = 0; gi < 4; ++gi) {
+    const int J = 2 * gi;
+    const int A = (P.colour[J] >> 1) & 1;
+    const int nxj = P.need[J][0], nyj = P.need[J][1];
 #pragma unroll
-    for (int k = 0; k < RR; ++k) U[a][k][0] = U[a][k][1] = 0.0;
-  double2 fcur[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
-  double2 fnext[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    for (int h = 0; h < G::RT / 2; ++h) {
+      const int r = r0 + A + 2 * h, gy = gy0 + r;
+      const bool rok = r >= G::GY - nyj && r < G::GY + TYo + nyj && gy >= 1 && gy <= ny;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int lx = 2 * lane + s;
+        const bool cok = lx >= G::GX - nxj && lx < G::GX + TXo + nxj && gx + s >= 1 && gx + s <= nx;
+        okbits |= (rok && cok) ? (1u << (4 * gi + 2 * h + s)) : 0u;
+      }
+    }
+  }
+  // owned output rows (the tiles partition [0, S) in x and y)
+  const bool colown = 2 * lane >= G::GX && 2 * lane < G::GX + TXo;
+  bool own[G::RT], fok[G::RT];
+  int64_t rowoff[G::RT];
+#pragma unroll
+  for (int a = 0; a < G::RT; ++a) {
+    const int r = r0 + a, gy = gy0 + r;
+    own[a] = colown && r >= G::GY && r < G::GY + TYo;
+    rowoff[a] = (int64_t)gy * p.sy + gx;
+    fok[a] = gy >= 0 && gy < Sy && gx >= 0 && gx + 1 < Sx;
+  }
 
-  // f of the two groups processed at step t: (row a, plane pz) for a pair
-  auto load_f = [&](int t, double2 (&fv)[2]) {
+  constexpr int RT = G::RT, H = RT / 2;
+  double U[RT][R][2];   // [row][ring][col]
+#pragma unroll
+  for (int a = 0; a < RT; ++a)
+#pragma unroll
+    for (int k = 0; k < R; ++k) U[a][k][0] = U[a][k][1] = 0.0;
+  double2 fcur[2][H], fnext[2][H];
+#pragma unroll
+  for (int gi = 0; gi < 2; ++gi)
+#pragma unroll
+    for (int h = 0; h < H; ++h) fcur[gi][h] = fnext[gi][h] = make_double2(0.0, 0.0);
+
+  // f of the two groups processed at step t (plane parity Q of t)
+  auto load_f = [&](int t, int Q, double2 (&fv)[2][H]) {
     if (FORM != 1) return;
-    const int q = (t - 1 + p.pz) & 1;                    // plane parity at step t
-    const int a = q;                                     // row r0 (q=0) or r0+1 (q=1)
-    const int pzs[2] = {q == 0 ? t : t - 1, q == 0 ? t - 3 : t - 4};
-    const int gy = gy0 + r0 + a;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int pz = pzs[k];
-      const bool ok = pz >= 1 && pz <= nz && gy >= 1 && gy <= ny && gx >= 0 && gx + 1 < Sx;
-      fv[k] = ok ? __ldg(reinterpret_cast<const double2 *>(p.f + (int64_t)pz * sz + (int64_t)gy * sy + gx))
-                 : make_double2(0.0, 0.0);
+    for (int gi = 0; gi < 2; ++gi) {
+      const int J = Q == 0 ? (gi == 0 ? 0 : 4) : (gi == 0 ? 2 : 6);
+      const int A = (P.colour[J] >> 1) & 1;
+      const int pz = t - P.lag[J];
+      const bool zin = pz >= 0 && pz < Sz;
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        fv[gi][h] = (fok[A + 2 * h] && zin)
+                        ? __ldg(reinterpret_cast<const double2 *>(p.f + (int64_t)pz * sz + rowoff[A + 2 * h]))
+                        : make_double2(0.0, 0.0);
     }
   };
-  load_f(t_begin, fcur);
+  load_f(t_begin, 0, fcur);
 
-  const int lrow0 = r0 * G::PX + 2 * lane;  // element offset of (row r0, col 2*lane) in a slot
+  double *me = su + r0 * G::PX + 2 * lane;  // (slot 0, row r0, col 2*lane)
   // compact Q1 order: index 0 = (-1,-1,-1) corner, 1 = (0,-1,-1) edge
-  const double wC = p.w[0], wE = p.w[1], awC = p.aw[0], awE = p.aw[1];
-  unsigned bad = 0;
-  for (int t0 = t_begin; t0 <= t_end; t0 += RR) {
+  const double wC = FORM == 0 ? p.aw[0] : p.w[0];
+  const double wE = FORM == 0 ? p.aw[1] : p.w[1];
+  unsigned emax = 0;   // max exponent field of any used update (0x7ff00000 = non-finite)
+
+  int ph = 0;
+  for (int t0 = t_begin; t0 <= t_end; t0 += R, ph ^= 1) {
     [&]<int... Ks>(std::integer_sequence<int, Ks...>) {
       (
           [&] {
             constexpr int KS = Ks;
+            constexpr int Q = KS & 1;  // plane parity of step t
             const int t = t0 + KS;
-            constexpr int Q = KS & 1;  // plane parity of t
-            load_f(t + 1, fnext);
-            // ---- plane t+1: wait for its TMA, take this thread's two rows ----
-            const int slot_t1 = so[D];  // so[k] = slot of plane t+1+D-k
-            mbar_wait3(mb_s + 8u * (uint32_t)(slot_t1 / G::SLOTE), parity_of(t + 1));
-            {
-              constexpr int R1 = (KS + 1) % RR;
+            load_f(t + 1, Q ^ 1, fnext);
+            // ---- plane t+1 (ring entry / slot KS) ----
+            mbar_wait3(mb_s + 8u * KS, (uint32_t)ph);
 #pragma unroll
-              for (int a = 0; a < 2; ++a) {
-                const double2 v = *reinterpret_cast<const double2 *>(su + slot_t1 + lrow0 + a * G::PX);
-                U[a][R1][0] = v.x;
-                U[a][R1][1] = v.y;
-              }
+            for (int a = 0; a < RT; ++a) {
+              const double2 v = *reinterpret_cast<const double2 *>(me + KS * G::SLOTE + a * G::PX);
+              U[a][KS][0] = v.x;
+              U[a][KS][1] = v.y;
             }
-            // ---- the two active colour groups of this step ----
+            // ---- the two independent colour groups of this step ----
+            double out[2][H][2];
+            bool ok[2][H][2];
             [&]<int... Gs>(std::integer_sequence<int, Gs...>) {
               (
                   [&] {
-                    constexpr int GI = Gs;                       // 0: first group, 1: second
+                    constexpr int GI = Gs;
                     constexpr int J = Q == 0 ? (GI == 0 ? 0 : 4) : (GI == 0 ? 2 : 6);
                     constexpr int LAG = P.lag[J];
-                    constexpr int A = (P.colour[J] >> 1) & 1;     // this group's row (y parity)
-                    constexpr int nxj = P.need[J][0], nyj = P.need[J][1], nzj = P.need[J][2];
+                    constexpr int A = (P.colour[J] >> 1) & 1;    // rows A, A + 2, ...
+                    constexpr int nzj = P.need[J][2];
+                    constexpr int RC = (KS - 1 - LAG + 2 * R) % R;  // ring entry / slot of plane pz
                     const int pz = t - LAG;
-                    if (pz < 1 || pz > nz || pz < z0 - nzj || pz >= z1 + nzj) return;
-                    constexpr int RC = ((KS - LAG) % RR + RR) % RR;        // ring slot of plane pz
-                    constexpr int RM = (RC + RR - 1) % RR, RP = (RC + 1) % RR;
-                    const int sc = so[D + 1 + LAG];                // smem slot of pz
-                    const int sm_ = so[D + 2 + LAG], sp = so[D + LAG];
-                    // other-warp row: above row r0 (A = 0) or below row r0+1 (A = 1)
-                    const int orow = A == 0 ? -1 : 2;              // relative to r0
-                    // accumulate plane by plane (dz outer = canonical order), so only one
-                    // plane's 3 x 4 window of values is live at a time
-                    const double uc0 = U[A][RC][0], uc1 = U[A][RC][1];
-                    double acc0 = acc_init<FORM, UNIT>(uc0, p), acc1 = acc_init<FORM, UNIT>(uc1, p);
+                    const bool okz = pz >= 1 && pz <= nz && pz >= z0 - nzj && pz < z1 + nzj;
+                    double acc[H][2];
+#pragma unroll
+                    for (int h = 0; h < H; ++h)
+#pragma unroll
+                      for (int s = 0; s < 2; ++s) acc[h][s] = acc_init<FORM, UNIT>(U[A + 2 * h][RC][s], p);
 #pragma unroll
                     for (int dz = -1; dz <= 1; ++dz) {
-                      const int ring = dz < 0 ? RM : (dz > 0 ? RP : RC);
-                      const int slot = dz < 0 ? sm_ : (dz > 0 ? sp : sc);
-                      double w[3][4];  // [dy+1][col+1]
+                      const int rs = (RC + dz + R) % R;   // compile-time after unrolling
+                      // rows A-1 .. A+RT-1 (relative to r0) of plane pz+dz, cols -1 .. 2
+                      double w[RT + 1][4];
 #pragma unroll
-                      for (int dy = -1; dy <= 1; ++dy) {
-                        if (dz == 0 && dy == 0) continue;  // no in-plane face/centre terms
-                        const int d = A + dy;              // row relative to r0
-                        if (d == orow) {
-                          const double *pr = su + slot + lrow0 + d * G::PX;
-                          const double2 m = *reinterpret_cast<const double2 *>(pr);
-                          w[dy + 1][0] = pr[-1];
-                          w[dy + 1][1] = m.x;
-                          w[dy + 1][2] = m.y;
-                          w[dy + 1][3] = pr[2];
+                      for (int i = 0; i <= RT; ++i) {
+                        const int d = A - 1 + i;
+                        if (dz == 0 && ((d - A) & 1) == 0) continue;  // no in-plane face/centre rows
+                        double lo, hi;
+                        if (d >= 0 && d < RT) {
+                          lo = U[d][rs][0];
+                          hi = U[d][rs][1];
                         } else {
-                          const double lo = U[d][ring][0], hi = U[d][ring][1];
-                          w[dy + 1][0] = __shfl_up_sync(0xffffffffu, hi, 1);
-                          w[dy + 1][1] = lo;
-                          w[dy + 1][2] = hi;
-                          w[dy + 1][3] = __shfl_down_sync(0xffffffffu, lo, 1);
+                          const double2 m = *reinterpret_cast<const double2 *>(me + rs * G::SLOTE + d * G::PX);
+                          lo = m.x;
+                          hi = m.y;
                         }
+                        w[i][0] = __shfl_up_sync(0xffffffffu, hi, 1);
+                        w[i][1] = lo;
+                        w[i][2] = hi;
+                        w[i][3] = __shfl_down_sync(0xffffffffu, lo, 1);
                       }
 #pragma unroll
                       for (int q = 0; q < shape_nnz(Q1); ++q) {
                         const Off o = shape_off(Q1, q);
                         if (o.z != dz) continue;
-                        // Q1 weights take two values (edges, corners; checked on the
-                        // host), held in two registers instead of 20 parameters
+                        // two weight values (edges, corners; checked on the host)
                         const bool corner = o.x != 0 && o.y != 0 && o.z != 0;
-                        const double wq = FORM == 0 ? (corner ? awC : awE) : (corner ? wC : wE);
-                        const double v0 = w[o.y + 1][o.x + 1], v1 = w[o.y + 1][o.x + 2];
-                        acc0 = __dadd_rn(acc0, __dmul_rn(wq, v0));
-                        acc1 = __dadd_rn(acc1, __dmul_rn(wq, v1));
+                        const double wq = corner ? wC : wE;
+#pragma unroll
+                        for (int h = 0; h < H; ++h)
+#pragma unroll
+                          for (int s = 0; s < 2; ++s) {
+                            const double v = w[2 * h + 1 + o.y][o.x + 1 + s];
+                            if (FORM == 0)
+                              acc[h][s] = __dadd_rn(acc[h][s], UNIT ? v : __dmul_rn(wq, v));
+                            else if (UNIT)
+                              acc[h][s] = __dsub_rn(acc[h][s], v);
+                            else
+                              acc[h][s] = __dadd_rn(acc[h][s], __dmul_rn(wq, v));
+                          }
                       }
                     }
-                    const double2 fc = fcur[GI];
-                    const bool rok = rowok(r0 + A, nyj);
-                    bool ok[2];
-                    double out[2];
-                    ok[0] = rok && colok(0, nxj);
-                    ok[1] = rok && colok(1, nxj);
-                    out[0] = acc_finish_used<FORM, UNIT, DIV>(acc0, uc0, fc.x, ok[0], p);
-                    out[1] = acc_finish_used<FORM, UNIT, DIV>(acc1, uc1, fc.y, ok[1], p);
+                    // division by w_c; exact fallback per warp, only for used lanes
+                    bool slow = false;
+                    double a[H][2], q[H][2];
 #pragma unroll
-                    for (int s = 0; s < 2; ++s)
-                      if (ok[s]) U[A][RC][s] = out[s];
-                    // publish the pair for the warps above/below (same values if not updated)
-                    *reinterpret_cast<double2 *>(su + sc + lrow0 + A * G::PX) = make_double2(U[A][RC][0], U[A][RC][1]);
+                    for (int h = 0; h < H; ++h)
+#pragma unroll
+                      for (int s = 0; s < 2; ++s) {
+                        ok[GI][h][s] = okz && ((okbits >> (2 * J + 2 * h + s)) & 1u);
+                        a[h][s] = FORM == 0 ? acc[h][s]
+                                            : __dsub_rn(s == 0 ? fcur[GI][h].x : fcur[GI][h].y, acc[h][s]);
+                        if (DIV == DIV_RCP) {
+                          const double e = __dmul_rn(a[h][s], p.rwc);
+                          q[h][s] = __fma_rn(__fma_rn(-p.wc, e, a[h][s]), p.rwc, e);
+                          const unsigned xe = ((unsigned)__double2hiint(a[h][s]) >> 20) & 0x7ffu;
+                          slow |= ok[GI][h][s] && (xe - 64u) >= 1919u;
+                        } else if (DIV == DIV_POW2) {
+                          q[h][s] = __dmul_rn(a[h][s], p.rwc);
+                        } else {
+                          q[h][s] = q1_div_exact(a[h][s], p.wc);
+                        }
+                      }
+                    if (DIV == DIV_RCP && __builtin_expect(__any_sync(0xffffffffu, slow), 0)) {
+#pragma unroll
+                      for (int h = 0; h < H; ++h)
+#pragma unroll
+                        for (int s = 0; s < 2; ++s) {
+                          const unsigned xe = ((unsigned)__double2hiint(a[h][s]) >> 20) & 0x7ffu;
+                          if (ok[GI][h][s] && (xe - 64u) >= 1919u) q[h][s] = q1_div_exact(a[h][s], p.wc);
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < H; ++h)
+#pragma unroll
+                      for (int s = 0; s < 2; ++s)
+                        out[GI][h][s] = FORM == 0 ? q[h][s]
+                                                  : __dadd_rn(U[A + 2 * h][RC][s], __dmul_rn(p.omega, q[h][s]));
+                  }(),
+                  ...);
+            }(std::make_integer_sequence<int, 2>{});
+            // ---- commit both groups: ring, non-finite tally, publish to smem ----
+            [&]<int... Gs>(std::integer_sequence<int, Gs...>) {
+              (
+                  [&] {
+                    constexpr int GI = Gs;
+                    constexpr int J = Q == 0 ? (GI == 0 ? 0 : 4) : (GI == 0 ? 2 : 6);
+                    constexpr int LAG = P.lag[J];
+                    constexpr int A = (P.colour[J] >> 1) & 1;
+                    constexpr int RC = (KS - 1 - LAG + 2 * R) % R;
+#pragma unroll
+                    for (int h = 0; h < H; ++h) {
+#pragma unroll
+                      for (int s = 0; s < 2; ++s) {
+                        const unsigned ex = (unsigned)__double2hiint(out[GI][h][s]) & 0x7ff00000u;
+                        emax = max(emax, ok[GI][h][s] ? ex : 0u);
+                        U[A + 2 * h][RC][s] = ok[GI][h][s] ? out[GI][h][s] : U[A + 2 * h][RC][s];
+                      }
+                      *reinterpret_cast<double2 *>(me + RC * G::SLOTE + (A + 2 * h) * G::PX) =
+                          make_double2(U[A + 2 * h][RC][0], U[A + 2 * h][RC][1]);
+                    }
                   }(),
                   ...);
             }(std::make_integer_sequence<int, 2>{});
             // ---- plane t - LAGMAX is final: owned pairs of both rows -> dst ----
             {
-              const int pz = t - G::LAGMAX;
-              constexpr int RO = ((KS - G::LAGMAX) % RR + RR) % RR;
-              if (pz >= z0 && pz < z1 && 2 * lane >= G::GX && 2 * lane < G::GX + TXo) {
+              constexpr int RO = (KS - 1 - G::LAGMAX + 2 * R) % R;
+              const int po = t - G::LAGMAX;
+              if (po >= z0 && po < z1) {
 #pragma unroll
-                for (int a = 0; a < 2; ++a) {
-                  const int r = r0 + a, gy = gy0 + r;
-                  if (r >= G::GY && r < G::GY + TYo) {
-                    const bool in_yz = pz >= 1 && pz <= nz && gy >= 1 && gy <= ny;
-                    bad |= (in_yz && gx >= 1 && ((unsigned)__double2hiint(U[a][RO][0]) & 0x7ff00000u) == 0x7ff00000u) |
-                           (in_yz && gx + 1 <= nx && ((unsigned)__double2hiint(U[a][RO][1]) & 0x7ff00000u) == 0x7ff00000u);
-                    stg_pair(dst + (int64_t)pz * sz + (int64_t)gy * sy + gx, U[a][RO][0], U[a][RO][1]);
-                  }
-                }
+                for (int a = 0; a < RT; ++a)
+                  if (own[a]) stg_pair(dst + (int64_t)po * sz + rowoff[a], U[a][RO][0], U[a][RO][1]);
               }
             }
             __syncthreads();
-            // rotate the slots; refill the slot of plane t-5 with plane t+2+D
-            {
-              const int tmp = so[WS - 1];
-#pragma unroll
-              for (int k = WS - 1; k > 0; --k) so[k] = so[k - 1];
-              so[0] = tmp;
-            }
+            // the slot of plane t-5 is free: refill it with plane t+3
             if (threadIdx.x == 0) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              issue(t + 2 + D);
+              issue(t + 3);
             }
-            fcur[0] = fnext[0];
-            fcur[1] = fnext[1];
+#pragma unroll
+            for (int gi = 0; gi < 2; ++gi)
+#pragma unroll
+              for (int h = 0; h < H; ++h) fcur[gi][h] = fnext[gi][h];
           }(),
           ...);
-    }(std::make_integer_sequence<int, RR>{});
+    }(std::make_integer_sequence<int, R>{});
   }
   if (threadIdx.x == 0) {  // drain the copies still in flight
-    const int tl = t_begin + ((t_end - t_begin) / RR + 1) * RR;
-    for (int k = 1; k <= 1 + D; ++k) {
+    const int tl = t_begin + ((t_end - t_begin) / R + 1) * R;  // first step not run
+    for (int k = 1; k <= 2; ++k) {
       const int pl = tl + k;
-      mbar_wait3(mb_s + 8u * (uint32_t)(((pl % WS) + WS) % WS), parity_of(pl));
+      mbar_wait3(mb_s + 8u * (uint32_t)((pl - base) & (R - 1)), (uint32_t)(((pl - base) / R) & 1));
     }
   }
   __syncthreads();
-  if (bad) atomicOr(p.status, 1);
+  if (__any_sync(0xffffffffu, emax == 0x7ff00000u) && lane == 0) atomicOr(p.status, 1);
 }
 
 }  // namespace sl
