@@ -462,8 +462,8 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
       if (e != cudaSuccess) return e;
     }
     CUtensorMap tmu, tmf;
-    cudaError_t e = make_tmap3(&tmu, src, p);
-    if (e == cudaSuccess) e = make_tmap3(&tmf, FORM == 1 ? p.f : src, p);
+    cudaError_t e = make_tmap3(&tmu, src, p, G::PX, G::BOXY);
+    if (e == cudaSuccess) e = make_tmap3(&tmf, FORM == 1 ? p.f : src, p, G::PX, G::BOXY);
     if (e != cudaSuccess) return e;
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
     const int64_t ntx = (Sx + G::TX - 1) / G::TX, nty = (Sy + G::TY - 1) / G::TY;
