@@ -86,6 +86,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
       : "memory");
 }
 
+// Exact division out of line (rare fallback of the Markstein fast path).
+__device__ __noinline__ double strip_div_exact(double a, double b) { return __ddiv_rn(a, b); }
+
 template <int S, int FORM, bool UNIT, int DIV, int M>
 __global__ void __launch_bounds__(32 * GeoS2<S, M>::WPB)
 k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, int64_t nstrip,
@@ -150,11 +153,19 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
   __syncwarp();
 
   int rlo[G::K], rhi[G::K];
+  unsigned colok = 0;  // bit (J * NC + cc): lane column cc is in phase J's need window and the interior
 #pragma unroll
   for (int j = 0; j < G::K; ++j) {
     rlo[j] = max(1, y0 - P.need[j][1]);
     rhi[j] = min(ny, y1 - 1 + P.need[j][1]);
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      const int lx = lx0 + cc;
+      if (lx >= G::GX - P.need[j][0] && lx < G::GX + TXo + P.need[j][0] && gx + cc >= 1 && gx + cc <= nx)
+        colok |= 1u << (j * NC + cc);
+    }
   }
+  static_assert(G::K * NC <= 32, "validity bits");
 
   double uu[NRR][NC], ff[NRR][NC];
 #pragma unroll
@@ -204,7 +215,7 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                     } else {
                       constexpr int s = 1 ^ (G::RB ? ((c + qy) & 1) : (c & 1));  // x parity
                       const int row = t - P.lag[J];
-                      if (row < rlo[J] || row > rhi[J]) return;
+                      const bool rok = row >= rlo[J] && row <= rhi[J];   // warp-uniform
                       // the lane's NP points of this colour: local columns 2k + s
                       double vl[3], vr[3];  // left / right ghost column from the adjacent lanes
                       constexpr int RRW[3] = {RM, R0, RP};
@@ -215,37 +226,55 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                         if (s == 1 && G::uses(1, dy - 1))
                           vr[dy] = __shfl_down_sync(0xffffffffu, uu[RRW[dy]][0], 1);
                       }
-                      double outv[NP];
-                      bool valid[NP];
+                      double xv[NP], qv[NP];
+                      bool valid[NP], slow = false;
 #pragma unroll
                       for (int k = 0; k < NP; ++k) {
                         const int cc = 2 * k + s;  // lane-local column of the point
-                        const int lx = lx0 + cc;
-                        valid[k] = lx >= G::GX - P.need[J][0] && lx < G::GX + TXo + P.need[J][0] &&
-                                   gx + cc >= 1 && gx + cc <= nx;
+                        valid[k] = rok && ((colok >> (J * NC + cc)) & 1u);
                         auto val = [&](int dy, int dx) -> double {
                           const int col = cc + dx;
                           if (col < 0) return vl[dy];
                           if (col >= NC) return vr[dy];
                           return uu[RRW[dy]][col];
                         };
-                        const double uc = uu[R0][cc];
-                        double acc = acc_init<FORM, UNIT>(uc, p);
+                        double acc = acc_init<FORM, UNIT>(uu[R0][cc], p);
 #pragma unroll
                         for (int q = 0; q < NNZ; ++q) {
                           const Off o = shape_off(S, q);
-                          acc = acc_add<FORM, UNIT>(acc, val(o.y + 1, o.x), q, p);
+                          const double v = val(o.y + 1, o.x);
+                          if (FORM == 0)
+                            acc = __dadd_rn(acc, UNIT ? v : __dmul_rn(p.aw[q], v));
+                          else
+                            acc = UNIT ? __dsub_rn(acc, v) : __dadd_rn(acc, __dmul_rn(p.w[q], v));
                         }
-                        if (FORM == 0) {
-                          outv[k] = div_wc_used<DIV>(acc, valid[k], p);
+                        xv[k] = FORM == 0 ? acc : __dsub_rn(ff[R0][cc], acc);
+                        if (DIV == DIV_RCP) {
+                          const double e = __dmul_rn(xv[k], p.rwc);
+                          qv[k] = __fma_rn(__fma_rn(-p.wc, e, xv[k]), p.rwc, e);
+                          const unsigned xe = ((unsigned)__double2hiint(xv[k]) >> 20) & 0x7ffu;
+                          slow |= valid[k] && (xe - 64u) >= 1919u;
+                        } else if (DIV == DIV_POW2) {
+                          qv[k] = __dmul_rn(xv[k], p.rwc);
                         } else {
-                          const double qd = div_wc_used<DIV>(__dsub_rn(ff[R0][cc], acc), valid[k], p);
-                          outv[k] = __dadd_rn(uc, __dmul_rn(p.omega, qd));
+                          qv[k] = strip_div_exact(xv[k], p.wc);
+                        }
+                      }
+                      // exact fallback, per warp, only for used lanes
+                      if (DIV == DIV_RCP && __builtin_expect(__any_sync(0xffffffffu, slow), 0)) {
+#pragma unroll
+                        for (int k = 0; k < NP; ++k) {
+                          const unsigned xe = ((unsigned)__double2hiint(xv[k]) >> 20) & 0x7ffu;
+                          if (valid[k] && (xe - 64u) >= 1919u) qv[k] = strip_div_exact(xv[k], p.wc);
                         }
                       }
 #pragma unroll
-                      for (int k = 0; k < NP; ++k)
-                        if (valid[k]) uu[R0][2 * k + s] = outv[k];
+                      for (int k = 0; k < NP; ++k) {
+                        const int cc = 2 * k + s;
+                        const double uc = uu[R0][cc];
+                        const double out = FORM == 0 ? qv[k] : __dadd_rn(uc, __dmul_rn(p.omega, qv[k]));
+                        uu[R0][cc] = valid[k] ? out : uc;
+                      }
                     }
                   }(),
                   ...);
