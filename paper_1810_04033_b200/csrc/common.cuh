@@ -143,6 +143,36 @@ __device__ __forceinline__ double acc_finish_used(double acc, double uc, double 
   return __dadd_rn(uc, __dmul_rn(p.omega, q));
 }
 
+// Exact division kept out of line: the fallback of the fast paths below.
+static __device__ __noinline__ double div_exact_ool(double a, double b) { return __ddiv_rn(a, b); }
+
+// As div_wc_used, for warp-convergent callers only: the fallback is taken for
+// the whole warp at once (one vote) and runs out of line, so the hot loop has
+// no divergent branch and no inlined division sequence.
+template <int DIV>
+__device__ __forceinline__ double div_wc_warp(double a, bool used, const Params &p) {
+  if (DIV == DIV_POW2) return __dmul_rn(a, p.rwc);
+  if (DIV == DIV_RCP) {
+    const unsigned e = ((unsigned)__double2hiint(a) >> 20) & 0x7ffu;
+    const double q0 = __dmul_rn(a, p.rwc);
+    const double r = __fma_rn(-p.wc, q0, a);
+    double q = __fma_rn(r, p.rwc, q0);
+    const bool slow = used && (e - 64u) >= 1919u;
+    if (__builtin_expect(__any_sync(0xffffffffu, slow), 0))
+      if (slow) q = div_exact_ool(a, p.wc);
+    return q;
+  }
+  return div_exact_ool(a, p.wc);
+}
+
+template <int FORM, bool UNIT, int DIV>
+__device__ __forceinline__ double acc_finish_warp(double acc, double uc, double fc, bool used,
+                                                  const Params &p) {
+  if (FORM == 0) return div_wc_warp<DIV>(acc, used, p);
+  const double q = div_wc_warp<DIV>(__dsub_rn(fc, acc), used, p);
+  return __dadd_rn(uc, __dmul_rn(p.omega, q));
+}
+
 __device__ __forceinline__ bool finite64(double v) {
   // exponent bits not all ones
   return (__double_as_longlong(v) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;

@@ -141,7 +141,7 @@ __device__ __forceinline__ unsigned update_item(const RowOff &ro, const FOff &fv
     }
     double fc = 0.0;
     if (FORM == 1) fc = fv(r, s);
-    out[r] = acc_finish_used<FORM, UNIT, DIV>(acc, uc, fc, (vmask >> r) & 1, p);
+    out[r] = acc_finish_warp<FORM, UNIT, DIV>(acc, uc, fc, (vmask >> r) & 1, p);  // warp-uniform callers
   }
   unsigned bad = 0;
 #pragma unroll
@@ -545,7 +545,23 @@ static cudaError_t launch_block2d(const Params &p, const double *src, double *ds
     if (e != cudaSuccess) return e;
   }
   const int64_t Sx = p.nx + 2, Sy = p.ny + 2;
-  const int ntx = (int)((Sx + G::TX - 1) / G::TX), nty = (int)((Sy + G::TY - 1) / G::TY);
+  // Tile count: at least what the maximal tile needs; more (smaller) tiles
+  // when that fills idle SMs of the wave — cost = waves x work per tile incl. ghost.
+  const int ntx0 = (int)((Sx + G::TX - 1) / G::TX), nty0 = (int)((Sy + G::TY - 1) / G::TY);
+  int ntx = ntx0, nty = nty0;
+  double best = 1e300;
+  for (int a = ntx0; a <= ntx0 + 8; ++a)
+    for (int b = nty0; b <= nty0 + 32; ++b) {
+      const int64_t waves = ((int64_t)a * b + slots - 1) / slots;
+      const double w = 2.0 * (double)((Sx / 2 + a - 1) / a) + 2 * G::GX;
+      const double h = (double)((Sy + b - 1) / b) + 2 * G::GY;
+      const double cost = (double)waves * w * h;
+      if (cost < best * 0.999) {
+        best = cost;
+        ntx = a;
+        nty = b;
+      }
+    }
   kern<<<(unsigned)(ntx * nty), G::NT, G::SMEM, st>>>(p, src, dst, ntx, nty);
   note_launch();
   return cudaGetLastError();
@@ -569,9 +585,10 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
   cudaError_t e = cudaSuccess;
   if (!stream_only && block2d_preferred(key, p)) {
     // FD5: 4 sweeps per pass, FE9: 2 (ghost 8 columns); remainder 1 at a time
-    const int mk = key.shape == FD5 ? 4 : 2;
+    // (8 FD5 sweeps per pass measured slower: ghost and phase count outgrow the saved passes)
     for (int s = 0; s < sweeps && e == cudaSuccess;) {
-      const int m = sweeps - s >= mk ? mk : 1;
+      const int left = sweeps - s;
+      const int m = key.shape == FD5 ? (left >= 4 ? 4 : 1) : (left >= 2 ? 2 : 1);
       e = dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
         if constexpr (S == FD5)
           return m == 4 ? launch_block2d<S, F, U, D, 4>(p, bufs[cur], bufs[cur ^ 1], st)
