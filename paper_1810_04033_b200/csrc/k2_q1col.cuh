@@ -149,13 +149,13 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   // owned output rows (the tiles partition [0, S) in x and y)
   const bool colown = 2 * lane >= G::GX && 2 * lane < G::GX + TXo;
   unsigned ownbits = 0, fokbits = 0;
-  int64_t rowoff[RT];
+  const int64_t rowoff0 = (int64_t)(gy0 + r0) * p.sy + gx;   // row r0 of this thread
+  const int sy32 = (int)p.sy;
 #pragma unroll
   for (int a = 0; a < RT; ++a) {
     const int r = r0 + a, gy = gy0 + r;
     ownbits |= (colown && r >= G::GY && r < G::GY + TYo) ? (1u << a) : 0u;
     fokbits |= (gy >= 0 && gy < Sy && gx >= 0 && gx + 1 < Sx) ? (1u << a) : 0u;
-    rowoff[a] = (int64_t)gy * p.sy + gx;
   }
 
   // own rows of planes pp-2 .. pp+1: [row][ring][col]; plane P at (P - base) % RR
@@ -178,16 +178,25 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
     for (int k = 2; k < RR; ++k) U[a][k][0] = U[a][k][1] = 0.0;
 
   // f of group gi at plane pz (rows A + 2h)
+  // f rows of group gi at plane pz (rows A + 2h).  Issued by volatile asm so
+  // each load stays where it is placed: two groups ahead of its use, never
+  // sunk next to a consumer of an earlier load.
+  const double *fthr = p.f + rowoff0;
   auto load_f = [&](int gi, int pz, double2 (&fv)[H]) {
     const int A = gi & 1;
     const bool zin = pz >= 0 && pz < Sz;
 #pragma unroll
-    for (int h = 0; h < H; ++h)
-      fv[h] = (FORM == 1 && ((fokbits >> (A + 2 * h)) & 1u) && zin)
-                  ? __ldg(reinterpret_cast<const double2 *>(p.f + (int64_t)pz * sz + rowoff[A + 2 * h]))
-                  : make_double2(0.0, 0.0);
+    for (int h = 0; h < H; ++h) {
+      fv[h] = make_double2(0.0, 0.0);
+      if (FORM == 1 && ((fokbits >> (A + 2 * h)) & 1u) && zin) {
+        const double *fp = fthr + (int64_t)pz * sz + (A + 2 * h) * sy32;
+        asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(fv[h].x), "=d"(fv[h].y) : "l"(fp));
+      }
+    }
   };
-  double2 f0[H], f1[H];   // G0 / G1 right-hand sides, loaded one pair step ahead
+  // f of G0 / G1 is loaded after G2 / G3 of the previous pair step, f of
+  // G2 / G3 after G0 / G1 of the same step
+  double2 f0[H], f1[H], f2[H], f3[H];
   load_f(0, p_begin, f0);
   load_f(1, p_begin, f1);
 
@@ -213,12 +222,20 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
     for (int dz = -1; dz <= 1; ++dz) {
       const int rs = (RC + dz + RR) % RR;
       const double *pl = slot_of(pz + dz);
-      // rows A-1 .. A+RT-1 (relative to r0) of plane pz+dz, cols -1 .. 2
-      double w[RT + 1][4];
+      // rows A-1 .. A+RT-1 (relative to r0) of plane pz+dz, cols -1 .. 2, as
+      // weighted products: each value is multiplied once per weight it is
+      // used with and the product is shared by the (up to four) points that
+      // read it — the same rounded w_j * u_j the canonical sum adds.  Rows of
+      // the other y parity on planes z+-1 feed corners and edges (pc, pe),
+      // the rest edges only; x+-1 columns arrive by shuffle as products.
+      // Rows are visited in order and each row's terms are added as soon as
+      // its products exist: per point the terms still arrive in canonical
+      // (y, then x ascending) order, and only one row of products is live.
 #pragma unroll
       for (int i = 0; i <= RT; ++i) {
         const int d = A - 1 + i;
-        if (dz == 0 && ((d - A) & 1) == 0) continue;  // no in-plane face/centre rows
+        const bool odd = ((d - A) & 1) != 0;
+        if (dz == 0 && !odd) continue;  // no in-plane face/centre rows
         double lo, hi;
         if (d >= 0 && d < RT) {
           lo = U[d][rs][0];
@@ -228,30 +245,38 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
           lo = m.x;
           hi = m.y;
         }
-        w[i][0] = __shfl_up_sync(0xffffffffu, hi, 1);
-        w[i][1] = lo;
-        w[i][2] = hi;
-        w[i][3] = __shfl_down_sync(0xffffffffu, lo, 1);
-      }
+        double pe[4], pc[4];
+        pe[1] = UNIT ? lo : __dmul_rn(wE, lo);
+        pe[2] = UNIT ? hi : __dmul_rn(wE, hi);
+        if (!UNIT && odd && dz != 0) {
+          pc[1] = __dmul_rn(wC, lo);
+          pc[2] = __dmul_rn(wC, hi);
+          pc[0] = __shfl_up_sync(0xffffffffu, pc[2], 1);
+          pc[3] = __shfl_down_sync(0xffffffffu, pc[1], 1);
+        } else {
+          pe[0] = __shfl_up_sync(0xffffffffu, pe[2], 1);
+          pe[3] = __shfl_down_sync(0xffffffffu, pe[1], 1);
+          pc[0] = pe[0];
+          pc[1] = pe[1];
+          pc[2] = pe[2];
+          pc[3] = pe[3];
+        }
 #pragma unroll
-      for (int q = 0; q < shape_nnz(Q1); ++q) {
-        const Off o = shape_off(Q1, q);
-        if (o.z != dz) continue;
-        // two weight values (edges, corners; checked on the host)
-        const bool corner = o.x != 0 && o.y != 0 && o.z != 0;
-        const double wq = corner ? wC : wE;
+        for (int h = 0; h < H; ++h) {
+          const int oy = i - (2 * h + 1);
+          if (oy < -1 || oy > 1) continue;
 #pragma unroll
-        for (int h = 0; h < H; ++h)
+          for (int q = 0; q < shape_nnz(Q1); ++q) {
+            const Off o = shape_off(Q1, q);
+            if (o.z != dz || o.y != oy) continue;
+            const bool corner = o.x != 0 && o.y != 0 && o.z != 0;
 #pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const double v = w[2 * h + 1 + o.y][o.x + 1 + s];
-            if (FORM == 0)
-              acc[h][s] = __dadd_rn(acc[h][s], UNIT ? v : __dmul_rn(wq, v));
-            else if (UNIT)
-              acc[h][s] = __dsub_rn(acc[h][s], v);
-            else
-              acc[h][s] = __dadd_rn(acc[h][s], __dmul_rn(wq, v));
+            for (int s = 0; s < 2; ++s) {
+              const double v = corner ? pc[o.x + 1 + s] : pe[o.x + 1 + s];
+              acc[h][s] = (FORM == 1 && UNIT) ? __dsub_rn(acc[h][s], v) : __dadd_rn(acc[h][s], v);
+            }
           }
+        }
       }
     }
     // division by w_c; exact fallback per warp, only for used lanes
@@ -308,10 +333,6 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
             constexpr int RP0 = (2 + 2 * KS) % RR;      // ring entry of the pair plane pp
             constexpr int RP1 = (RP0 + 1) % RR, RM1 = (RP0 + RR - 1) % RR;
             const int pp = pp0 + 2 * KS;
-            // G2 / G3 right-hand sides (plane pp-1), needed after two barriers
-            double2 f2[H], f3[H];
-            load_f(2, pp - 1, f2);
-            load_f(3, pp - 1, f3);
             // planes pp and pp+1 -> ring
             wait_plane(pp);
             wait_plane(pp + 1);
@@ -328,7 +349,7 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
               }
             }
             group.template operator()<0, RP0>(pp, f0);
-            load_f(0, pp + 2, f0);
+            load_f(2, pp - 1, f2);
             __syncthreads();
             // everybody is past the previous pair step: refill the slots of
             // planes pp-4, pp-3 with planes pp+4, pp+5
@@ -338,11 +359,13 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
               issue(pp + 5);
             }
             group.template operator()<1, RP0>(pp, f1);
-            load_f(1, pp + 2, f1);
+            load_f(3, pp - 1, f3);
             __syncthreads();
             group.template operator()<2, RP0>(pp, f2);
+            load_f(0, pp + 2, f0);
             __syncthreads();
             group.template operator()<3, RP0>(pp, f3);
+            load_f(1, pp + 2, f1);
             // planes pp-1 and pp are final: owned rows -> dst
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
@@ -353,7 +376,7 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
                   if ((ownbits >> a) & 1u) {
                     const double lo = k == 0 ? U[a][RM1][0] : U[a][RP0][0];
                     const double hi = k == 0 ? U[a][RM1][1] : U[a][RP0][1];
-                    stg_pair(dst + (int64_t)po * sz + rowoff[a], lo, hi);
+                    stg_pair(dst + (int64_t)po * sz + rowoff0 + a * sy32, lo, hi);
                   }
               }
             }
