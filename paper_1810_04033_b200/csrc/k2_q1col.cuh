@@ -16,10 +16,13 @@
 // a chunk of z; 12 warps.  Thread (warp w, lane i) owns column pair (2i, 2i+1)
 // of the RT = 4 tile rows r0 = 4w + delta .. r0 + 3, where delta makes row r0
 // a y-parity 0 row, so each group updates 2 x 2 points of the thread (rows A,
-// A + 2).  The thread keeps its rows of planes p-2 .. p+1 in a register ring;
-// only the row of the warp above/below comes from the plane's shared-memory
-// slot, and the x+-1 columns from warp shuffles.  Every update is published to
-// the slot for the neighbouring warps.
+// A + 2).  The thread keeps its rows of planes p-2 .. p in a register ring
+// (plane p+1, read only by G0/G1, comes from its slot); otherwise only the
+// row of the warp above/below comes from the plane's shared-memory slot, and
+// the x+-1 columns from warp shuffles.  Neighbour values enter the sums as
+// weighted products computed once per value and weight and shared (by
+// shuffle) with the lanes that need them.  Every update is published to the
+// slot for the neighbouring warps.
 //
 // u planes arrive by TMA (64 x 49 x 1 boxes, zero-filled out of range) into
 // 8 smem slots, up to six planes ahead.  The loop is unrolled by two pair
@@ -46,13 +49,14 @@ struct Q1Geo {
   static constexpr int BOXY = PY + 1;                     // rows loaded (delta shift)
   static constexpr int TX = PX - 2 * GX, TY = PY - 2 * GY;
   static constexpr int S = 8;                             // smem slots
-  static constexpr int RR = 4;                            // register ring: planes p-2 .. p+1
+  static constexpr int RR = 4;                            // ring entries (planes p-2 .. p live)
   static constexpr int RT = 4;                            // tile rows per thread
   static constexpr int NT = 32 * PY / RT;                 // 384
   static constexpr int LAGMAX = 1;
   static constexpr int SLOTE = PX * BOXY;
   static constexpr int LEADE = 2 * PX;                    // guard rows before slot 0
-  static constexpr size_t SMEM = size_t(LEADE + S * SLOTE + 2 * PX) * sizeof(double) + S * 8;
+  static constexpr int FBUFE = 2 * (RT / 2) * 2 * NT;      // f staging: 2 buffers x H rows x 2 cols
+  static constexpr size_t SMEM = size_t(LEADE + S * SLOTE + 2 * PX + FBUFE) * sizeof(double) + S * 8;
   static_assert(P.load[0] <= GX && P.load[1] <= GY && P.load[2] <= GZ, "ghost margin");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
@@ -73,7 +77,8 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   constexpr int RT = G::RT, H = RT / 2, RR = G::RR;
   extern __shared__ __align__(128) double qsm[];
   double *su = qsm + G::LEADE;  // slot k at su + k*SLOTE
-  uint64_t *mb = reinterpret_cast<uint64_t *>(su + G::S * G::SLOTE + 2 * G::PX);
+  double *fbuf = su + G::S * G::SLOTE + 2 * G::PX;   // [buffer][h][thread] double2
+  uint64_t *mb = reinterpret_cast<uint64_t *>(fbuf + G::FBUFE);
   const uint32_t su_s = (uint32_t)__cvta_generic_to_shared(su);
   const uint32_t mb_s = (uint32_t)__cvta_generic_to_shared(mb);
 
@@ -178,27 +183,33 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
     for (int k = 2; k < RR; ++k) U[a][k][0] = U[a][k][1] = 0.0;
 
   // f of group gi at plane pz (rows A + 2h)
-  // f rows of group gi at plane pz (rows A + 2h).  Issued by volatile asm so
-  // each load stays where it is placed: two groups ahead of its use, never
-  // sunk next to a consumer of an earlier load.
+  // f rows of group gi at plane pz (rows A + 2h) are staged per thread in
+  // shared memory by cp.async, one group ahead of their use, alternating
+  // between two buffers (the groups of a pair step use buffers 0, 1, 0, 1).
+  // cp.async.wait_group waits for exactly the older copies, so the newest
+  // copy in flight never delays a consumer (a register LDG would share its
+  // scoreboard with it).  Masked rows are zero-filled (src size 0).
   const double *fthr = p.f + rowoff0;
-  auto load_f = [&](int gi, int pz, double2 (&fv)[H]) {
+  const uint32_t fb_s = (uint32_t)__cvta_generic_to_shared(fbuf) + 16u * threadIdx.x;
+  auto issue_f = [&](int gi, int pz, int buf) {
     const int A = gi & 1;
     const bool zin = pz >= 0 && pz < Sz;
 #pragma unroll
     for (int h = 0; h < H; ++h) {
-      fv[h] = make_double2(0.0, 0.0);
-      if (FORM == 1 && ((fokbits >> (A + 2 * h)) & 1u) && zin) {
-        const double *fp = fthr + (int64_t)pz * sz + (A + 2 * h) * sy32;
-        asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(fv[h].x), "=d"(fv[h].y) : "l"(fp));
-      }
+      const bool live = FORM == 1 && ((fokbits >> (A + 2 * h)) & 1u) && zin;
+      const double *fp = live ? fthr + (int64_t)pz * sz + (A + 2 * h) * sy32 : p.u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(fb_s + 16u * (buf * H + h) * G::NT),
+                   "l"(fp), "r"(live ? 16 : 0));
     }
+    asm volatile("cp.async.commit_group;");
   };
-  // f of G0 / G1 is loaded after G2 / G3 of the previous pair step, f of
-  // G2 / G3 after G0 / G1 of the same step
-  double2 f0[H], f1[H], f2[H], f3[H];
-  load_f(0, p_begin, f0);
-  load_f(1, p_begin, f1);
+  auto read_f = [&](int buf, double2 (&fv)[H]) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+#pragma unroll
+    for (int h = 0; h < H; ++h)
+      fv[h] = reinterpret_cast<const double2 *>(fbuf)[(buf * H + h) * G::NT + threadIdx.x];
+  };
+  if (FORM == 1) issue_f(0, p_begin, 0);
 
   // compact Q1 order: index 0 = (-1,-1,-1) corner, 1 = (0,-1,-1) edge
   const double wC = FORM == 0 ? p.aw[0] : p.w[0];
@@ -206,7 +217,14 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   unsigned emax = 0;   // max exponent field of any used update (0x7ff00000 = non-finite)
 
   // one colour group GI at plane pz = pp - (GI >> 1); RP = ring entry of pp
-  auto group = [&]<int GI, int RP>(int pp, const double2 (&fv)[H]) {
+  auto group = [&]<int GI, int RP>(int pp) {
+    // next group's right-hand side in flight, this group's from its buffer
+    double2 fv[H];
+    if (FORM == 1) {
+      constexpr int NGI = (GI + 1) & 3;
+      issue_f(NGI, GI == 0 ? pp : GI == 3 ? pp + 2 : pp - 1, NGI & 1);
+      read_f(GI & 1, fv);
+    }
     constexpr int A = GI & 1;                      // rows A, A + 2
     constexpr int LAGG = GI >> 1;
     constexpr int RC = (RP - LAGG + RR) % RR;      // ring entry of plane pz
@@ -237,7 +255,7 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
         const bool odd = ((d - A) & 1) != 0;
         if (dz == 0 && !odd) continue;  // no in-plane face/centre rows
         double lo, hi;
-        if (d >= 0 && d < RT) {
+        if (d >= 0 && d < RT && !(LAGG == 0 && dz == 1)) {
           lo = U[d][rs][0];
           hi = U[d][rs][1];
         } else {
@@ -331,25 +349,25 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
           [&] {
             constexpr int KS = Ks;                      // pair step within the ring turn
             constexpr int RP0 = (2 + 2 * KS) % RR;      // ring entry of the pair plane pp
-            constexpr int RP1 = (RP0 + 1) % RR, RM1 = (RP0 + RR - 1) % RR;
+            constexpr int RM1 = (RP0 + RR - 1) % RR;
             const int pp = pp0 + 2 * KS;
-            // planes pp and pp+1 -> ring
+            // planes pp-1 and pp -> ring (plane pp+1 is read from its slot:
+            // only three planes are ever live in registers)
             wait_plane(pp);
             wait_plane(pp + 1);
             {
-              const double *pa = slot_of(pp), *pb = slot_of(pp + 1);
+              const double *pa = slot_of(pp - 1), *pb = slot_of(pp);
 #pragma unroll
               for (int a = 0; a < RT; ++a) {
                 const double2 va = *reinterpret_cast<const double2 *>(pa + a * G::PX);
                 const double2 vb = *reinterpret_cast<const double2 *>(pb + a * G::PX);
-                U[a][RP0][0] = va.x;
-                U[a][RP0][1] = va.y;
-                U[a][RP1][0] = vb.x;
-                U[a][RP1][1] = vb.y;
+                U[a][RM1][0] = va.x;
+                U[a][RM1][1] = va.y;
+                U[a][RP0][0] = vb.x;
+                U[a][RP0][1] = vb.y;
               }
             }
-            group.template operator()<0, RP0>(pp, f0);
-            load_f(2, pp - 1, f2);
+            group.template operator()<0, RP0>(pp);
             __syncthreads();
             // everybody is past the previous pair step: refill the slots of
             // planes pp-4, pp-3 with planes pp+4, pp+5
@@ -358,14 +376,11 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
               issue(pp + 4);
               issue(pp + 5);
             }
-            group.template operator()<1, RP0>(pp, f1);
-            load_f(3, pp - 1, f3);
+            group.template operator()<1, RP0>(pp);
             __syncthreads();
-            group.template operator()<2, RP0>(pp, f2);
-            load_f(0, pp + 2, f0);
+            group.template operator()<2, RP0>(pp);
             __syncthreads();
-            group.template operator()<3, RP0>(pp, f3);
-            load_f(1, pp + 2, f1);
+            group.template operator()<3, RP0>(pp);
             // planes pp-1 and pp are final: owned rows -> dst
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
@@ -390,6 +405,7 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
     for (int pl = pl_end; pl <= pl_end + 3; ++pl) wait_plane(pl);
   }
   __syncthreads();
+  asm volatile("cp.async.wait_all;" ::: "memory");
   if (__any_sync(0xffffffffu, emax == 0x7ff00000u) && lane == 0) atomicOr(p.status, 1);
 }
 
