@@ -297,7 +297,9 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
         }
       }
     }
-    // division by w_c; exact fallback per warp, only for used lanes
+    // division by w_c.  The fast-path range test ignores the lane masks (a
+    // zero-filled point outside the grid only sends its warp into the
+    // fallback, which applies them), so no mask is kept live across it.
     bool ok[H][2], slow = false;
     double a[H][2], q[H][2];
 #pragma unroll
@@ -309,8 +311,8 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
         if (DIV == DIV_RCP) {
           const double e = __dmul_rn(a[h][s], p.rwc);
           q[h][s] = __fma_rn(__fma_rn(-p.wc, e, a[h][s]), p.rwc, e);
-          const unsigned xe = ((unsigned)__double2hiint(a[h][s]) >> 20) & 0x7ffu;
-          slow |= ok[h][s] && (xe - 64u) >= 1919u;
+          const unsigned xe = (unsigned)__double2hiint(a[h][s]) & 0x7ff00000u;
+          slow |= (xe - (64u << 20)) >= (1919u << 20);
         } else if (DIV == DIV_POW2) {
           q[h][s] = __dmul_rn(a[h][s], p.rwc);
         } else {
@@ -322,8 +324,8 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
       for (int h = 0; h < H; ++h)
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
-          const unsigned xe = ((unsigned)__double2hiint(a[h][s]) >> 20) & 0x7ffu;
-          if (ok[h][s] && (xe - 64u) >= 1919u) q[h][s] = q1_div_exact(a[h][s], p.wc);
+          const unsigned xe = (unsigned)__double2hiint(a[h][s]) & 0x7ff00000u;
+          if (ok[h][s] && (xe - (64u << 20)) >= (1919u << 20)) q[h][s] = q1_div_exact(a[h][s], p.wc);
         }
     }
     // commit: ring, non-finite tally, publish to the plane's slot
@@ -340,6 +342,18 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
       }
       *reinterpret_cast<double2 *>(pc + (A + 2 * h) * G::PX) =
           make_double2(U[A + 2 * h][RC][0], U[A + 2 * h][RC][1]);
+    }
+  };
+
+  // owned rows of a final plane (ring entry RE) -> dst
+  double *const dthr = dst + rowoff0;
+  auto store_plane = [&](int po, auto RE) {
+    constexpr int E = decltype(RE)::value;
+    if (po >= z0 && po < z1) {
+      double *dp = dthr + (int64_t)po * sz;
+#pragma unroll
+      for (int a = 0; a < RT; ++a)
+        if ((ownbits >> a) & 1u) stg_pair(dp + a * sy32, U[a][E][0], U[a][E][1]);
     }
   };
 
@@ -377,24 +391,12 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
               issue(pp + 5);
             }
             group.template operator()<1, RP0>(pp);
+            store_plane(pp, std::integral_constant<int, RP0>{});  // plane pp is final after G1
             __syncthreads();
             group.template operator()<2, RP0>(pp);
             __syncthreads();
             group.template operator()<3, RP0>(pp);
-            // planes pp-1 and pp are final: owned rows -> dst
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-              const int po = pp - 1 + k;
-              if (po >= z0 && po < z1) {
-#pragma unroll
-                for (int a = 0; a < RT; ++a)
-                  if ((ownbits >> a) & 1u) {
-                    const double lo = k == 0 ? U[a][RM1][0] : U[a][RP0][0];
-                    const double hi = k == 0 ? U[a][RM1][1] : U[a][RP0][1];
-                    stg_pair(dst + (int64_t)po * sz + rowoff0 + a * sy32, lo, hi);
-                  }
-              }
-            }
+            store_plane(pp - 1, std::integral_constant<int, RM1>{});
           }(),
           ...);
     }(std::make_integer_sequence<int, 2>{});
