@@ -107,6 +107,16 @@ SL_API size_t sl_workspace_bytes(const sl_grid *g, const sl_stencil *s);
 SL_API int sl_sweep(const sl_grid *g, const sl_stencil *s, int32_t sweeps, uint32_t flags,
              double *workspace, size_t workspace_bytes, int32_t *d_status, void *stream);
 
+/* One fused sweep from `src` to `dst` (two distinct buffers of g's layout;
+ * g->u is ignored) that writes only the planes [zbegin, zend) of the slowest
+ * axis (z in 3D, y in 2D) of dst and reads src around them.  The multi-GPU
+ * slab runner computes its boundary planes first and exchanges them while the
+ * interior pass runs (there is no reference counterpart: the reference is
+ * single-process).  SL_E_UNSUPPORTED when no streaming kernel covers the
+ * stencil/grid (odd row length, batch > 1, odd x origin). */
+SL_API int sl_sweep_pass(const sl_grid *g, const sl_stencil *s, const double *src, double *dst,
+                         int64_t zbegin, int64_t zend, int32_t *d_status, void *stream);
+
 /* One colour phase in place: one parallel_for pass of sweep_colouring
  * (strategies.py:374-393) / one colour of sweep_colouring_reference (:420-433). */
 SL_API int sl_colour_pass(const sl_grid *g, const sl_stencil *s, int32_t colour,

@@ -120,6 +120,8 @@ static int make_params(const sl_grid *g, const sl_stencil *s, int32_t *d_status,
   p->px = (int)(g->origin[0] & 1);
   p->py = (int)(g->origin[1] & 1);
   p->pz = g->dim == 3 ? (int)(g->origin[2] & 1) : 0;
+  p->zlo = 0;
+  p->zhi = (int32_t)(g->dim == 3 ? sz : sy);
   for (int j = 0; j < shape_nnz(key->shape); ++j) {
     const Off o = shape_off(key->shape, j);
     p->delta[j] = o.x + o.y * p->sy + o.z * p->sz;
@@ -237,6 +239,25 @@ int sl_sweep(const sl_grid *g, const sl_stencil *s, int32_t sweeps, uint32_t fla
       if (rc != SL_OK) return rc;
     }
   return SL_OK;
+}
+
+int sl_sweep_pass(const sl_grid *g, const sl_stencil *s, const double *src, double *dst, int64_t zbegin,
+                  int64_t zend, int32_t *d_status, void *stream) {
+  if (!g || !src || !dst || src == dst) return SL_E_INVAL;
+  sl_grid gs = *g;
+  gs.u = const_cast<double *>(src);
+  KernelKey key;
+  Params p;
+  int rc = make_params(&gs, s, d_status, &key, &p);
+  if (rc != SL_OK) return rc;
+  if (!d_status || zbegin < 0 || zend < zbegin || zend > p.zhi) return SL_E_INVAL;
+  if (empty_grid(p)) return SL_OK;
+  p.zlo = (int32_t)zbegin;
+  p.zhi = (int32_t)zend;
+  int handled = 0;
+  rc = cuda_status(launch_one_pass(key, p, src, dst, (cudaStream_t)stream, &handled));
+  if (rc != SL_OK) return rc;
+  return handled ? SL_OK : SL_E_UNSUPPORTED;
 }
 
 int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats, int64_t count,

@@ -83,6 +83,7 @@ struct Params {
   double aw[26];  // |w|
   double wc, rwc, omega;
   int64_t delta[26];  // flat deltas (update_cells / residual)
+  int32_t zlo, zhi;   // fused passes: output planes [zlo, zhi) of the slowest axis (z; y in 2D)
 };
 
 template <int FORM, bool UNIT, int DIV>

@@ -180,7 +180,8 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
   const int zc = item / (int)(tl.ntx * tl.nty);
   const int x0 = (int)tile_start(tx, Sx, tl.ntx), x1 = (int)tile_start(tx + 1, Sx, tl.ntx);
   const int y0 = (int)chunk_start(ty, Sy, tl.nty), y1 = (int)chunk_start(ty + 1, Sy, tl.nty);
-  const int z0 = (int)chunk_start(zc, Sz, tl.nzc), z1 = (int)chunk_start(zc + 1, Sz, tl.nzc);
+  const int z0 = p.zlo + (int)chunk_start(zc, p.zhi - p.zlo, tl.nzc);
+  const int z1 = p.zlo + (int)chunk_start(zc + 1, p.zhi - p.zlo, tl.nzc);
   const int TXo = x1 - x0, TYo = y1 - y0;
   const int gx0 = x0 - G::GX, gy0 = y0 - G::GY;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -434,7 +435,7 @@ static cudaError_t launch_stream3d(const Params &p, const double *src, double *d
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
     tl.ntx = (Sx + G::TX - 1) / G::TX;
     tl.nty = (Sy + G::TY - 1) / G::TY;
-    tl.nzc = pick_chunks(tl.ntx * tl.nty, Sz, slots, G::GZ + G::LAGMAX + 1, 16);
+    tl.nzc = pick_chunks(tl.ntx * tl.nty, p.zhi - p.zlo, slots, G::GZ + G::LAGMAX + 1, 16);
     const int64_t items = tl.ntx * tl.nty * tl.nzc;
     kern<<<(unsigned)items, G::NT, G::SMEM, st>>>(p, src, dst, tl);
     note_launch();
@@ -467,7 +468,7 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     if (e != cudaSuccess) return e;
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
     const int64_t ntx = (Sx + G::TX - 1) / G::TX, nty = (Sy + G::TY - 1) / G::TY;
-    const int64_t nzc = pick_chunks(ntx * nty, Sz, slots, G::GZ + G::LAGMAX + G::R, 16);
+    const int64_t nzc = pick_chunks(ntx * nty, p.zhi - p.zlo, slots, G::GZ + G::LAGMAX + G::R, 16);
     kern<<<(unsigned)(ntx * nty * nzc), G::NT, G::SMEM, st>>>(p, tmu, tmf, dst, ntx, nty, nzc);
     note_launch();
     return cudaGetLastError();
@@ -485,7 +486,7 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     if (e != cudaSuccess) return e;
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
     const int64_t ntx = (Sx + G::TX - 1) / G::TX, nty = (Sy + G::TY - 1) / G::TY;
-    const int64_t nzc = pick_chunks(ntx * nty, Sz, slots, G::GZ + G::LAGMAX + G::RR, 16);
+    const int64_t nzc = pick_chunks(ntx * nty, p.zhi - p.zlo, slots, G::GZ + G::LAGMAX + G::RR, 16);
     kern<<<(unsigned)(ntx * nty * nzc), G::NT, G::SMEM, st>>>(p, tmu, dst, ntx, nty, nzc);
     note_launch();
     return cudaGetLastError();
@@ -501,7 +502,7 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     }
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2;
     const int64_t nstrip = (Sx + G::TX - 1) / G::TX;
-    const int64_t nchunk = pick_chunks(nstrip, Sy, slots * G::WPB, G::GY + G::LAGMAX + G::U, 16);
+    const int64_t nchunk = pick_chunks(nstrip, p.zhi - p.zlo, slots * G::WPB, G::GY + G::LAGMAX + G::U, 16);
     const int64_t warps = nstrip * nchunk;
     const int64_t blocks = (warps + G::WPB - 1) / G::WPB;
     kern<<<(unsigned)blocks, 32 * G::WPB, G::SMEM, st>>>(p, src, dst, nstrip, nchunk);
@@ -565,6 +566,18 @@ static cudaError_t launch_block2d(const Params &p, const double *src, double *ds
   kern<<<(unsigned)(ntx * nty), G::NT, G::SMEM, st>>>(p, src, dst, ntx, nty);
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_one_pass(const KernelKey &key, const Params &p, const double *src, double *dst,
+                            cudaStream_t st, int *handled) {
+  *handled = 0;
+  if (p.batch > 1 || !fused_supported(key, p)) return cudaSuccess;
+  if (((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaSuccess;
+  *handled = 1;
+  if (p.zhi <= p.zlo) return cudaSuccess;
+  return dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
+    return launch_pass<S, F, U, D, 1>(p, src, const_cast<double *>(dst), st);
+  });
 }
 
 cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, double *workspace,

@@ -12,4 +12,10 @@ size_t fused_workspace_bytes(const KernelKey &key, const Params &p);
 cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, double *workspace,
                          size_t workspace_bytes, cudaStream_t st, int *handled, bool stream_only);
 
+// One fused single-sweep pass src -> dst writing only the slowest-axis planes
+// [p.zlo, p.zhi) of dst (the slab runner's boundary / interior split).
+// *handled = 0 when no streaming pass kernel covers this stencil and grid.
+cudaError_t launch_one_pass(const KernelKey &key, const Params &p, const double *src, double *dst,
+                            cudaStream_t st, int *handled);
+
 }  // namespace sl

@@ -88,7 +88,8 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   const int tx = item % (int)ntx, ty = (item / (int)ntx) % (int)nty, zc = item / (int)(ntx * nty);
   const int x0 = (int)(2 * (((int64_t)tx * (Sx / 2)) / ntx)), x1 = (int)(2 * (((int64_t)(tx + 1) * (Sx / 2)) / ntx));
   const int y0 = (int)(((int64_t)ty * Sy) / nty), y1 = (int)(((int64_t)(ty + 1) * Sy) / nty);
-  const int z0 = (int)(((int64_t)zc * Sz) / nzc), z1 = (int)(((int64_t)(zc + 1) * Sz) / nzc);
+  const int zlen = p.zhi - p.zlo;
+  const int z0 = p.zlo + (int)(((int64_t)zc * zlen) / nzc), z1 = p.zlo + (int)(((int64_t)(zc + 1) * zlen) / nzc);
   const int TXo = x1 - x0, TYo = y1 - y0;
   const int gx0 = x0 - G::GX, gy0 = y0 - G::GY;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

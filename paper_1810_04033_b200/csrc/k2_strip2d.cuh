@@ -108,7 +108,9 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
   const int strip = (int)(wid % nstrip), chunk = (int)(wid / nstrip);
   const int x0 = (int)(2 * (((int64_t)strip * (Sx / 2)) / nstrip));
   const int x1 = (int)(2 * (((int64_t)(strip + 1) * (Sx / 2)) / nstrip));
-  const int y0 = (int)(((int64_t)chunk * Sy) / nchunk), y1 = (int)(((int64_t)(chunk + 1) * Sy) / nchunk);
+  const int ylen = p.zhi - p.zlo;  // output rows [zlo, zhi): the slowest axis of a 2D grid
+  const int y0 = p.zlo + (int)(((int64_t)chunk * ylen) / nchunk);
+  const int y1 = p.zlo + (int)(((int64_t)(chunk + 1) * ylen) / nchunk);
   const int TXo = x1 - x0;
   constexpr int NP = G::NP, NC = 2 * NP;  // pairs / columns per lane
   const int gxs = x0 - G::GX;            // global x of the strip's column 0 (even)

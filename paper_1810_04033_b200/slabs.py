@@ -12,6 +12,13 @@ use).  Planes are contiguous in the reference layout, so every exchange is a
 plain contiguous send/recv (NCCL P2P over NVLink on GPUs, gloo on CPU in the
 tests); the only collective is the final gather.
 
+Each sweep is one fused pass between two slab buffers (`sl_sweep_pass`, no
+copy back).  The last sweep of a round writes only the owned planes: first
+the G+1 planes at each end, whose exchange with the neighbours then starts
+(NCCL runs on its own stream after the boundary passes) while the interior
+pass runs on the compute stream; the ghost planes of the new state are the
+received ones, so they are never recomputed.
+
 Correctness contract: after every exchange each rank holds the global state
 on [a - G - 1, b + G + 1]; the gathered result equals the 1-rank result bit
 for bit (tests/test_slabs.py, world size 2 on gloo).
@@ -108,10 +115,12 @@ class SlabRunner:
         self.shape = (nl + 2, s) if dim == 2 else (nl + 2, s, s)
         self.device = torch.device(device) if device is not None else torch.device("cpu")
         self.u = torch.zeros(self.shape, dtype=torch.float64, device=self.device)
+        self._u2 = torch.zeros_like(self.u)   # the other buffer of the pass ping-pong
         self.f = None
         self.omega = None
-        self._compute = compute or self._gpu_compute
-        self._ws = None
+        self._pass = compute or self._gpu_pass   # (src, dst, z0, z1): one sweep into dst planes [z0, z1)
+        self._desc = None
+        self._fused = None
         self._status = None
 
     # -- inputs -----------------------------------------------------------------
@@ -134,6 +143,7 @@ class SlabRunner:
         sl = (slice(g0 - L.lo, g1 - L.lo + 1),) + (slice(1, n + 1),) * (self.dim - 1)
         u[sl] = vals
         self.u.copy_(torch.from_numpy(u))
+        self._u2.copy_(self.u)
         if rhs_seed is not None:
             f = np.zeros(self.shape)
             f[sl] = _rng_slice(rhs_seed, (g0 - 1) * inner, cnt, "uniform").reshape(vals.shape)
@@ -146,6 +156,7 @@ class SlabRunner:
         import torch
         L = self.layout
         self.u.copy_(torch.as_tensor(np.ascontiguousarray(u_global[L.lo:L.hi + 1])))
+        self._u2.copy_(self.u)
         if f_global is not None:
             self.f = torch.as_tensor(np.ascontiguousarray(f_global[L.lo:L.hi + 1])).to(self.device)
             self.omega = float(omega)
@@ -153,35 +164,64 @@ class SlabRunner:
 
     # -- sweeping ---------------------------------------------------------------
 
-    def _gpu_compute(self, sweeps: int):
+    def _descriptors(self):
+        """(grid, stencil) descriptors of the local slab (u is set per call)."""
+        if self._desc is None:
+            g = _native.SlGrid()
+            g.dim = self.dim
+            g.n[0] = self.n
+            if self.dim == 2:
+                g.n[1] = self.layout.local_interior
+                g.origin[1] = self.layout.lo
+            else:
+                g.n[1] = self.n
+                g.n[2] = self.layout.local_interior
+                g.origin[2] = self.layout.lo
+            g.batch = 1
+            g.batch_stride = self.u.numel()
+            form, omega = _native.SL_FORM_R, 0.0
+            if self.f is not None:
+                g.f = self.f.data_ptr()
+                form, omega = _native.SL_FORM_D, self.omega
+            self._desc = (g, self.kind.descriptor(form, omega))
+        return self._desc
+
+    def _gpu_pass(self, src, dst, z0: int, z1: int):
         import torch
         lib = _native.require_cuda()
-        g = _native.SlGrid()
-        g.dim = self.dim
-        g.n[0] = self.n
-        if self.dim == 2:
-            g.n[1] = self.layout.local_interior
-            g.origin[1] = self.layout.lo
-        else:
-            g.n[1] = self.n
-            g.n[2] = self.layout.local_interior
-            g.origin[2] = self.layout.lo
-        g.batch = 1
-        g.batch_stride = self.u.numel()
-        g.u = self.u.data_ptr()
-        form, omega = _native.SL_FORM_R, 0.0
-        if self.f is not None:
-            g.f = self.f.data_ptr()
-            form, omega = _native.SL_FORM_D, self.omega
-        st = self.kind.descriptor(form, omega)
+        g, st = self._descriptors()
         if self._status is None:
             self._status = torch.zeros(1, dtype=torch.int32, device=self.device)
-        nb = lib.sl_workspace_bytes(ctypes.byref(g), ctypes.byref(st))
-        if nb and (self._ws is None or self._ws.numel() * 8 < nb):
-            self._ws = torch.empty((nb + 7) // 8, dtype=torch.float64, device=self.device)
-        ws_ptr = self._ws.data_ptr() if nb else None
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        rc = lib.sl_sweep(ctypes.byref(g), ctypes.byref(st), sweeps, 0, ws_ptr, nb,
+        rc = lib.sl_sweep_pass(ctypes.byref(g), ctypes.byref(st), src.data_ptr(), dst.data_ptr(),
+                               z0, z1, self._status.data_ptr(), stream)
+        _native.check(rc, "slab pass")
+
+    def _gpu_fused(self) -> bool:
+        """Whether a streaming pass kernel covers this slab (an empty plane
+        window probes it without launching)."""
+        if self._fused is None:
+            import torch
+            lib = _native.require_cuda()
+            g, st = self._descriptors()
+            if self._status is None:
+                self._status = torch.zeros(1, dtype=torch.int32, device=self.device)
+            rc = lib.sl_sweep_pass(ctypes.byref(g), ctypes.byref(st), self.u.data_ptr(),
+                                   self._u2.data_ptr(), 0, 0, self._status.data_ptr(), None)
+            if rc not in (_native.SL_OK, _native.SL_E_UNSUPPORTED):
+                _native.check(rc, "slab pass")
+            self._fused = rc == _native.SL_OK
+        return self._fused
+
+    def _gpu_inplace(self, k: int):
+        """k sweeps in place with the per-colour kernels (grids no streaming
+        pass kernel covers, e.g. an odd row length)."""
+        import torch
+        lib = _native.require_cuda()
+        g, st = self._descriptors()
+        g.u = self.u.data_ptr()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        rc = lib.sl_sweep(ctypes.byref(g), ctypes.byref(st), k, 0, None, 0,
                           self._status.data_ptr(), stream)
         _native.check(rc, "slab sweep")
 
@@ -190,21 +230,55 @@ class SlabRunner:
             self._status.zero_()
             raise NumericsError("non-finite update in a slab sweep")
 
-    def exchange(self):
-        """Boundary planes to/from the neighbouring slabs (contiguous views)."""
-        if self.world == 1:
-            return
+    def _exchange_ops(self, buf):
         import torch.distributed as dist
         L, G = self.layout, self.layout.ghost
         ops = []
         if self.rank > 0:   # lower neighbour: send my [a, a+G], receive its [a-G-1, a-1]
-            ops.append(dist.P2POp(dist.isend, self.u[L.a - L.lo:L.a - L.lo + G + 1], self.rank - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, self.u[0:L.a - L.lo], self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.isend, buf[L.a - L.lo:L.a - L.lo + G + 1], self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf[0:L.a - L.lo], self.rank - 1, self.group))
         if self.rank < self.world - 1:   # upper: send my [b-G, b], receive [b+1, b+G+1]
-            ops.append(dist.P2POp(dist.isend, self.u[L.b - G - L.lo:L.b - L.lo + 1], self.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, self.u[L.b + 1 - L.lo:], self.rank + 1, self.group))
-        for req in dist.batch_isend_irecv(ops):
+            ops.append(dist.P2POp(dist.isend, buf[L.b - G - L.lo:L.b - L.lo + 1], self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, buf[L.b + 1 - L.lo:], self.rank + 1, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def exchange(self):
+        """Boundary planes of the current state to/from the neighbouring slabs."""
+        if self.world == 1:
+            return
+        for req in self._exchange_ops(self.u):
             req.wait()
+
+    def _swap(self):
+        self.u, self._u2 = self._u2, self.u
+
+    def compute_round(self, k: int, exchange: bool = False):
+        """k sweeps of the slab (k <= ghost_sweeps); with `exchange`, the
+        boundary planes of the result are traded with the neighbours while
+        the interior pass runs.  Without it the ghost planes of the result
+        are left for the caller to fill (tests emulate the exchange)."""
+        L, G = self.layout, self.layout.ghost
+        if self._pass == self._gpu_pass and not self._gpu_fused():
+            self._gpu_inplace(k)
+            if exchange:
+                self.exchange()
+            return
+        whole = self.shape[0]
+        for _ in range(k - 1):   # redundant sweeps of the whole local slab
+            self._pass(self.u, self._u2, 0, whole)
+            self._swap()
+        a, b = L.a - L.lo, L.b - L.lo          # owned planes, local indices
+        if self.world == 1 or b - a + 1 <= 2 * (G + 1):
+            self._pass(self.u, self._u2, a, b + 1)
+            reqs = self._exchange_ops(self._u2) if exchange and self.world > 1 else []
+        else:
+            self._pass(self.u, self._u2, a, a + G + 1)
+            self._pass(self.u, self._u2, b - G, b + 1)
+            reqs = self._exchange_ops(self._u2) if exchange else []
+            self._pass(self.u, self._u2, a + G + 1, b - G)   # overlaps the exchange
+        for req in reqs:
+            req.wait()
+        self._swap()
 
     def sweep(self, count: int, cost: CostModel = CostModel()):
         """`count` colour-ordered sweeps of the global grid (exchanging every
@@ -212,12 +286,14 @@ class SlabRunner:
         if not cost.is_free:
             raise NotImplementedError("slab sweeps run the k = 0 bandwidth path only; "
                                       "use a single-GPU mesh for the cost model")
+        # planes no pass writes (global halo) must agree in both buffers
+        self._u2[0].copy_(self.u[0])
+        self._u2[-1].copy_(self.u[-1])
         while count > 0:
             k = min(self.ghost_sweeps, count)
-            self._compute(k)
+            self.compute_round(k, exchange=True)
             count -= k
-            self.exchange()
-        if self._compute == self._gpu_compute:
+        if self._pass == self._gpu_pass:
             self.check_status()
 
     def owned(self):

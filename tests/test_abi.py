@@ -96,6 +96,15 @@ def test_invalid_arguments_rejected_before_launch():
     g.batch = 2
     g.batch_stride = 10                                           # overlapping grids
     assert _sweep(g, s) == _native.SL_E_INVAL
+    lib = _native.load()
+    st = ctypes.c_int32(0)
+    g = _grid()
+    src, dst = g.u, g.u + 4096
+    for a, b in ((-1, 3), (3, 2), (0, 10 ** 6)):                  # plane window out of range
+        assert lib.sl_sweep_pass(ctypes.byref(g), ctypes.byref(s), src, dst, a, b,
+                                 ctypes.addressof(st), None) == _native.SL_E_INVAL
+    assert lib.sl_sweep_pass(ctypes.byref(g), ctypes.byref(s), src, src, 0, 1,
+                             ctypes.addressof(st), None) == _native.SL_E_INVAL   # in place
 
 
 def test_cost_sweep_arguments_rejected_before_launch():

@@ -27,7 +27,7 @@ def _emulated(name, n, sweeps, world, per):
     while left > 0:
         k = min(per, left)
         for r in rs:
-            r._compute(k)
+            r.compute_round(k)
         left -= k
         for r0, r1 in zip(rs, rs[1:]):   # what exchange() sends, as device copies
             L0, L1, G = r0.layout, r1.layout, r0.layout.ghost
@@ -46,7 +46,8 @@ def _emulated(name, n, sweeps, world, per):
 
 @pytest.mark.parametrize("name,n,sweeps,world,per", [
     ("fd7", 40, 5, 2, 1), ("fd7", 37, 4, 3, 2), ("fe27q1", 30, 3, 2, 1),
-    ("fe9", 130, 4, 2, 1), ("fe9", 97, 5, 3, 2), ("fd5", 66, 6, 2, 2)])
+    ("fe9", 130, 4, 2, 1), ("fe9", 97, 5, 3, 2), ("fd5", 66, 6, 2, 2), ("fe27q1", 64, 3, 3, 1),
+    ("fd7", 70, 4, 4, 1), ("fe9", 200, 3, 4, 1)])
 def test_emulated_slabs_equal_single_domain(name, n, sweeps, world, per):
     dim = R.STENCIL_TABLE[name][0]
     want = R.init_u(dim, n, 7)

@@ -26,14 +26,16 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def oracle_compute(runner, name):
-    def run(k):
-        u = runner.u.numpy()
+def oracle_pass(runner, name):
+    """The slab pass contract on CPU: one sweep of src, planes [z0, z1) -> dst."""
+    def run(src, dst, z0, z1):
+        u = src.numpy().copy()
         f = runner.f.numpy() if runner.f is not None else None
         origin = [0, 0, 0]
         origin[runner.dim - 1] = runner.layout.lo
-        R.sweep(u, name, k, f=f, omega=runner.omega or 0.8, form="D" if f is not None else "R",
+        R.sweep(u, name, 1, f=f, omega=runner.omega or 0.8, form="D" if f is not None else "R",
                 origin=tuple(origin))
+        dst[z0:z1] = torch.from_numpy(u[z0:z1])
     return run
 
 
@@ -55,7 +57,7 @@ def _run(rank, world, case, q):
         kind = sl.get_stencil(name)
         r = SlabRunner(kind.dim, n, kind, world=world, rank=rank, ghost_sweeps=per,
                        ghost=2 * per)
-        r._compute = oracle_compute(r, name)
+        r._pass = oracle_pass(r, name)
         r.init(7, 8, 0.8)
         r.sweep(sweeps)
         out = r.gather()
@@ -64,7 +66,7 @@ def _run(rank, world, case, q):
 
 
 CASES = [("fd7", 11, 5, 2), ("fe9", 14, 4, 1), ("fe27q1", 10, 3, 1), ("fd5", 16, 6, 3), ("fd7", 20, 4, 4),
-         ("fd5", 9, 3, 1)]
+         ("fd5", 9, 3, 1), ("fd7", 24, 3, 1), ("fe27q1", 22, 2, 1)]   # the last two split boundary/interior
 
 
 @pytest.mark.parametrize("case", CASES)
