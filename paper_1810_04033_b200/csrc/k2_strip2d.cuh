@@ -33,14 +33,20 @@ struct GeoS2 {
   static constexpr bool RB = (P.C == 2);
   static constexpr int GX = (P.load[0] + 1) & ~1;
   static constexpr int GY = P.load[1];
-  static constexpr int NP = 1;                         // column pairs per lane
+#ifndef STRIP_NP
+#define STRIP_NP 2
+#endif
+#ifndef STRIP_WPB
+#define STRIP_WPB 2
+#endif
+  static constexpr int NP = STRIP_NP;                  // column pairs per lane
   static constexpr int WS = 64 * NP;                   // strip width (columns)
   static constexpr int TX = WS - 2 * GX;
   static constexpr int NRR0 = LAGMAX + 3;             // register ring: rows t-LAGMAX-1 .. t+1
   static constexpr int NRR = NRR0 <= 2 ? 2 : (NRR0 <= 4 ? 4 : 8);
   static constexpr int NS = 8;                         // smem ring slots (rows in flight)
   static constexpr int U = NRR > NS ? NRR : NS;        // unroll: multiple of both (powers of 2)
-  static constexpr int WPB = 2;                        // warps per block
+  static constexpr int WPB = STRIP_WPB;                // warps per block
   static constexpr int ROWB = WS * 8;                  // bytes of one array's row segment
   static constexpr int SLOTB = 2 * ROWB;               // u + f
   static constexpr size_t SMEM = size_t(WPB) * NS * SLOTB;
