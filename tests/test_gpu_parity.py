@@ -312,3 +312,51 @@ def test_lex_differs_from_colour_order():
     sl.sweep_serial(m1, sl.FD5, sl.CostModel())
     sl.run_sweeps(m2, sl.FD5, sl.CostModel(), 1)
     assert not _bits_equal(m1.values, m2.values)
+
+
+# -- single pass with an output plane window (slab runner building block) -----
+
+@pytest.mark.parametrize("name,n", [("fe27q1", 40), ("fd7", 37 + 1), ("fe9", 150), ("fd5", 130)])
+def test_sweep_pass_windows_compose(name, n):
+    """sl_sweep_pass over [0, a) + [a, b) + [b, S) along the slowest axis gives
+    the same dst as one pass over [0, S), and both equal one oracle sweep."""
+    import ctypes
+
+    import torch
+    kind = sl.get_stencil(name)
+    dim = kind.dim
+    u = R.init_u(dim, n, 5)
+    f = R.init_f(dim, n, 6)
+    lib = _native.require_cuda()
+    src = torch.from_numpy(u).cuda()
+    fd = torch.from_numpy(f).cuda()
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    g = _native.SlGrid()
+    g.dim = dim
+    for a in range(dim):
+        g.n[a] = n
+    g.batch = 1
+    g.batch_stride = src.numel()
+    g.u = src.data_ptr()
+    g.f = fd.data_ptr()
+    st = kind.descriptor(_native.SL_FORM_D, 0.8)
+    S = n + 2
+    whole = torch.zeros_like(src)
+    parts = torch.zeros_like(src)
+    stream = torch.cuda.current_stream().cuda_stream
+
+    def run(dst, z0, z1):
+        rc = lib.sl_sweep_pass(ctypes.byref(g), ctypes.byref(st), src.data_ptr(), dst.data_ptr(),
+                               z0, z1, status.data_ptr(), stream)
+        assert rc == _native.SL_OK, _native.load().sl_strerror(rc)
+
+    run(whole, 0, S)
+    a, b = S // 3, S // 3 + 5
+    for z0, z1 in ((b, S), (0, a), (a, b)):
+        run(parts, z0, z1)
+    torch.cuda.synchronize()
+    want = u.copy()
+    coracle.sweep(want, name, 1, f=f, omega=0.8, form="D")
+    assert _bits_equal(whole.cpu().numpy(), want)
+    assert _bits_equal(parts.cpu().numpy(), want)
+    assert int(status.item()) == 0
