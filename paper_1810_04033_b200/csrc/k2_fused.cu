@@ -442,6 +442,13 @@ static cudaError_t launch_stream3d(const Params &p, const double *src, double *d
     return cudaGetLastError();
 }
 
+// all neighbour weights of the shape equal (signed; |w| then equal too)
+static bool equal_weights(const Params &p, int shape) {
+  for (int j = 1; j < shape_nnz(shape); ++j)
+    if (p.w[j] != p.w[0]) return false;
+  return true;
+}
+
 // k2_q1col holds the Q1 weights as two values: all edges equal, all corners equal
 static bool q1_two_weights(const Params &p) {
   for (int j = 0; j < shape_nnz(Q1); ++j) {
@@ -494,19 +501,27 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     return launch_stream3d<S, FORM, UNIT, DIV, M>(p, src, dst, st);
   } else {
     using G = GeoS2<S, M>;
-    auto kern = k2_strip2d<S, FORM, UNIT, DIV, M>;
-    static thread_local int64_t slots = 0;  // resident blocks
-    if (!slots) {
-      cudaError_t e = prepare(kern, G::SMEM, 32 * G::WPB, &slots);
-      if (e != cudaSuccess) return e;
-    }
-    const int64_t Sx = p.nx + 2, Sy = p.ny + 2;
-    const int64_t nstrip = (Sx + G::TX - 1) / G::TX;
-    const int64_t nchunk = pick_chunks(nstrip, p.zhi - p.zlo, slots * G::WPB, G::GY + G::LAGMAX + G::U, 16);
-    const int64_t warps = nstrip * nchunk;
-    const int64_t blocks = (warps + G::WPB - 1) / G::WPB;
-    kern<<<(unsigned)blocks, 32 * G::WPB, G::SMEM, st>>>(p, src, dst, nstrip, nchunk);
-    note_launch();
+    auto run = [&](auto kern) -> cudaError_t {
+      static thread_local int64_t slots = 0;  // resident blocks (per kernel variant)
+      if (!slots) {
+        cudaError_t e = prepare(kern, G::SMEM, 32 * G::WPB, &slots);
+        if (e != cudaSuccess) return e;
+      }
+      const int64_t Sx = p.nx + 2;
+      const int64_t nstrip = (Sx + G::TX - 1) / G::TX;
+      const int64_t nchunk = pick_chunks(nstrip, p.zhi - p.zlo, slots * G::WPB, G::GY + G::LAGMAX + G::U, 16);
+      const int64_t warps = nstrip * nchunk;
+      const int64_t blocks = (warps + G::WPB - 1) / G::WPB;
+      kern<<<(unsigned)blocks, 32 * G::WPB, G::SMEM, st>>>(p, src, dst, nstrip, nchunk);
+      note_launch();
+      return cudaSuccess;
+    };
+    cudaError_t e;
+    if constexpr (S == FE9 && !UNIT)
+      e = equal_weights(p, S) ? run(k2_strip2d<S, FORM, UNIT, DIV, M, true>) : run(k2_strip2d<S, FORM, UNIT, DIV, M>);
+    else
+      e = run(k2_strip2d<S, FORM, UNIT, DIV, M>);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
 }

@@ -95,7 +95,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
 // Exact division out of line (rare fallback of the Markstein fast path).
 __device__ __noinline__ double strip_div_exact(double a, double b) { return __ddiv_rn(a, b); }
 
-template <int S, int FORM, bool UNIT, int DIV, int M>
+// EQW: every neighbour weight equal (FE9: -1/3; host-checked).  Then each
+// value's product w * u is rounded once per phase and shared by the lane's
+// points and, through the shuffle, by the adjacent lane — the same rounded
+// terms, added in the same canonical order.
+template <int S, int FORM, bool UNIT, int DIV, int M, bool EQW = false>
 __global__ void __launch_bounds__(32 * GeoS2<S, M>::WPB)
 k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, int64_t nstrip,
            int64_t nchunk) {
@@ -227,12 +231,21 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                       // the lane's NP points of this colour: local columns 2k + s
                       double vl[3], vr[3];  // left / right ghost column from the adjacent lanes
                       constexpr int RRW[3] = {RM, R0, RP};
+                      // EQW: products of the lane's columns (unused ones are dead code)
+                      double pw[3][NC];
+                      const double w0 = FORM == 0 ? p.aw[0] : p.w[0];
+                      if constexpr (EQW) {
+#pragma unroll
+                        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+                          for (int c2 = 0; c2 < NC; ++c2) pw[dy][c2] = __dmul_rn(w0, uu[RRW[dy]][c2]);
+                      }
 #pragma unroll
                       for (int dy = 0; dy < 3; ++dy) {
                         if (s == 0 && G::uses(-1, dy - 1))
-                          vl[dy] = __shfl_up_sync(0xffffffffu, uu[RRW[dy]][NC - 1], 1);
+                          vl[dy] = __shfl_up_sync(0xffffffffu, EQW ? pw[dy][NC - 1] : uu[RRW[dy]][NC - 1], 1);
                         if (s == 1 && G::uses(1, dy - 1))
-                          vr[dy] = __shfl_down_sync(0xffffffffu, uu[RRW[dy]][0], 1);
+                          vr[dy] = __shfl_down_sync(0xffffffffu, EQW ? pw[dy][0] : uu[RRW[dy]][0], 1);
                       }
                       double xv[NP], qv[NP];
                       bool valid[NP], slow = false;
@@ -244,14 +257,16 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                           const int col = cc + dx;
                           if (col < 0) return vl[dy];
                           if (col >= NC) return vr[dy];
-                          return uu[RRW[dy]][col];
+                          return EQW ? pw[dy][col] : uu[RRW[dy]][col];
                         };
                         double acc = acc_init<FORM, UNIT>(uu[R0][cc], p);
 #pragma unroll
                         for (int q = 0; q < NNZ; ++q) {
                           const Off o = shape_off(S, q);
                           const double v = val(o.y + 1, o.x);
-                          if (FORM == 0)
+                          if (EQW)
+                            acc = __dadd_rn(acc, v);  // v is already w * u, rounded
+                          else if (FORM == 0)
                             acc = __dadd_rn(acc, UNIT ? v : __dmul_rn(p.aw[q], v));
                           else
                             acc = UNIT ? __dsub_rn(acc, v) : __dadd_rn(acc, __dmul_rn(p.w[q], v));
