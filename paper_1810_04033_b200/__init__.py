@@ -11,6 +11,7 @@ from .kernels import (FD5, FD7, FE9, FE27, FE27Q1, STENCILS, CostModel, Numerics
                       update_cells_batch)
 from .mesh import Mesh, init, init_rhs, make_mesh
 from .patches import PatchBatch, init_patches
+from .pipeline import SweepPipeline
 from .pool import DevicePool, Schedule, WorkerPool
 from .runner import (CONVERGENCE_TOL, BenchConfig, BenchResult, ConfigError, Report,
                      StrategyRunner, mesh_digest, parse_cost, run_benchmark, run_verification,
