@@ -185,6 +185,14 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
 #pragma unroll
     for (int j = 0; j < NC; ++j) uu[k][j] = ff[k][j] = 0.0;
 
+  // per-kernel constants in registers: without the opaque moves the compiler
+  // re-reads them from the constant bank (LDCU + R2UR) in every phase
+  double c_rwc, c_wc, c_om, c_w0;
+  asm("mov.b64 %0, %1;" : "=d"(c_rwc) : "d"(p.rwc));
+  asm("mov.b64 %0, %1;" : "=d"(c_wc) : "d"(p.wc));
+  asm("mov.b64 %0, %1;" : "=d"(c_om) : "d"(p.omega));
+  asm("mov.b64 %0, %1;" : "=d"(c_w0) : "d"(FORM == 0 ? p.aw[0] : p.w[0]));
+
   unsigned bad = 0;
   uint32_t round = 0;  // completed passes over the smem ring
   for (int t0 = t_begin; t0 <= t_end; t0 += G::U, round += G::U / NS) {
@@ -233,7 +241,7 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                       constexpr int RRW[3] = {RM, R0, RP};
                       // EQW: products of the lane's columns (unused ones are dead code)
                       double pw[3][NC];
-                      const double w0 = FORM == 0 ? p.aw[0] : p.w[0];
+                      const double w0 = c_w0;
                       if constexpr (EQW) {
 #pragma unroll
                         for (int dy = 0; dy < 3; ++dy)
@@ -273,12 +281,12 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                         }
                         xv[k] = FORM == 0 ? acc : __dsub_rn(ff[R0][cc], acc);
                         if (DIV == DIV_RCP) {
-                          const double e = __dmul_rn(xv[k], p.rwc);
-                          qv[k] = __fma_rn(__fma_rn(-p.wc, e, xv[k]), p.rwc, e);
+                          const double e = __dmul_rn(xv[k], c_rwc);
+                          qv[k] = __fma_rn(__fma_rn(-c_wc, e, xv[k]), c_rwc, e);
                           const unsigned xe = ((unsigned)__double2hiint(xv[k]) >> 20) & 0x7ffu;
                           slow |= valid[k] && (xe - 64u) >= 1919u;
                         } else if (DIV == DIV_POW2) {
-                          qv[k] = __dmul_rn(xv[k], p.rwc);
+                          qv[k] = __dmul_rn(xv[k], c_rwc);
                         } else {
                           qv[k] = strip_div_exact(xv[k], p.wc);
                         }
@@ -295,7 +303,7 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                       for (int k = 0; k < NP; ++k) {
                         const int cc = 2 * k + s;
                         const double uc = uu[R0][cc];
-                        const double out = FORM == 0 ? qv[k] : __dadd_rn(uc, __dmul_rn(p.omega, qv[k]));
+                        const double out = FORM == 0 ? qv[k] : __dadd_rn(uc, __dmul_rn(c_om, qv[k]));
                         uu[R0][cc] = valid[k] ? out : uc;
                       }
                     }
