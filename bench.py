@@ -287,7 +287,11 @@ def run_ours(args, wl, rank, world, local):
     elif world > 1 and wl.index in (2, 3, 4):
         # configs 2-4: slabs along the slowest axis, ghost planes exchanged by NCCL P2P
         from paper_1810_04033_b200.slabs import SlabRunner
-        sr = SlabRunner(wl.dim, wl.n, kind, world=world, rank=rank, ghost_sweeps=1, device=dev)
+        # 2D slabs are thin in work per sweep (config 2 at 8 GPUs: ~40 us): exchange every 5
+        # sweeps (5-sweep ghost rows, <2% redundant rows) so the host issues ~1.4 launches per
+        # sweep; 3D slabs exchange every sweep (a deeper z ghost would cost 6-12% extra planes)
+        sr = SlabRunner(wl.dim, wl.n, kind, world=world, rank=rank,
+                        ghost_sweeps=5 if wl.dim == 2 and wl.sweeps % 5 == 0 else 1, device=dev)
         sr.init(wl.seed, wl.seed + 1, wl.omega)
         total_updates, scaling = wl.updates, "strong"
         parallelism = f"slabs x{world} (axis {'z' if wl.dim == 3 else 'y'}, ghost {sr.layout.ghost}, NCCL P2P)"
