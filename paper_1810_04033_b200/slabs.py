@@ -13,11 +13,15 @@ plain contiguous send/recv (NCCL P2P over NVLink on GPUs, gloo on CPU in the
 tests); the only collective is the final gather.
 
 Each sweep is one fused pass between two slab buffers (`sl_sweep_pass`, no
-copy back).  The last sweep of a round writes only the owned planes: first
-the G+1 planes at each end, whose exchange with the neighbours then starts
-(NCCL runs on its own stream after the boundary passes) while the interior
-pass runs on the compute stream; the ghost planes of the new state are the
-received ones, so they are never recomputed.
+copy back).  The last sweep of a round writes only the owned planes; the
+ghost planes of the new state are the received ones, so they are never
+recomputed.  With `overlap=True` that last sweep runs as three launches —
+the G+1 planes at each end first, whose exchange then starts (NCCL runs on
+its own stream after the boundary passes) while the interior pass runs.  It
+is off by default: at the BASELINE sizes a 3-plane pass costs a full chunk
+warm-up, so the two extra launches cost more than the NVLink transfer they
+hide (measured compute per sweep at 8 slabs: config 3 157 vs 115 us,
+config 4 1106 vs 977 us, config 2 +13 %; the transfer is ~20 / ~70 / ~5 us).
 
 Correctness contract: after every exchange each rank holds the global state
 on [a - G - 1, b + G + 1]; the gathered result equals the 1-rank result bit
@@ -99,13 +103,15 @@ class SlabRunner:
     """One rank's slab of a dim-D grid of interior extent n (cubic)."""
 
     def __init__(self, dim: int, n: int, kind: StencilKind, world: int = 1, rank: int = 0,
-                 ghost_sweeps: int = 1, device=None, group=None, compute=None, ghost: int = None):
+                 ghost_sweeps: int = 1, device=None, group=None, compute=None, ghost: int = None,
+                 overlap: bool = False):
         import torch
         if kind.dim != dim:
             raise ValueError(f"{kind.name} is {kind.dim}D, not {dim}D")
         self.dim, self.n, self.kind = dim, n, kind
         self.world, self.rank, self.group = world, rank, group
         self.ghost_sweeps = ghost_sweeps
+        self.overlap = overlap   # boundary passes first, exchange during the interior pass
         g = ghost if ghost is not None else ghost_depth(kind, ghost_sweeps)
         self.layout = SlabLayout(n, world, rank, g)
         if world > 1:
@@ -268,7 +274,7 @@ class SlabRunner:
             self._pass(self.u, self._u2, 0, whole)
             self._swap()
         a, b = L.a - L.lo, L.b - L.lo          # owned planes, local indices
-        if self.world == 1 or b - a + 1 <= 2 * (G + 1):
+        if self.world == 1 or not self.overlap or b - a + 1 <= 2 * (G + 1):
             self._pass(self.u, self._u2, a, b + 1)
             reqs = self._exchange_ops(self._u2) if exchange and self.world > 1 else []
         else:

@@ -17,10 +17,10 @@ from paper_1810_04033_b200.slabs import SlabRunner
 pytestmark = pytest.mark.gpu
 
 
-def _emulated(name, n, sweeps, world, per):
+def _emulated(name, n, sweeps, world, per, overlap=False):
     kind = sl.get_stencil(name)
-    rs = [SlabRunner(kind.dim, n, kind, world=world, rank=r, ghost_sweeps=per, device="cuda")
-          for r in range(world)]
+    rs = [SlabRunner(kind.dim, n, kind, world=world, rank=r, ghost_sweeps=per, device="cuda",
+                     overlap=overlap) for r in range(world)]
     for r in rs:
         r.init(7, 8, 0.8)
     left = sweeps
@@ -48,12 +48,13 @@ def _emulated(name, n, sweeps, world, per):
     ("fd7", 40, 5, 2, 1), ("fd7", 37, 4, 3, 2), ("fe27q1", 30, 3, 2, 1),
     ("fe9", 130, 4, 2, 1), ("fe9", 97, 5, 3, 2), ("fd5", 66, 6, 2, 2), ("fe27q1", 64, 3, 3, 1),
     ("fd7", 70, 4, 4, 1), ("fe9", 200, 3, 4, 1)])
-def test_emulated_slabs_equal_single_domain(name, n, sweeps, world, per):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_emulated_slabs_equal_single_domain(name, n, sweeps, world, per, overlap):
     dim = R.STENCIL_TABLE[name][0]
     want = R.init_u(dim, n, 7)
     f = R.init_f(dim, n, 8)
     coracle.sweep(want, name, sweeps, f=f, omega=0.8, form="D")
-    got = _emulated(name, n, sweeps, world, per)
+    got = _emulated(name, n, sweeps, world, per, overlap)
     assert np.array_equal(got.view(np.int64), want.view(np.int64))
 
 

@@ -56,7 +56,7 @@ def _run(rank, world, case, q):
         name, n, sweeps, per = case
         kind = sl.get_stencil(name)
         r = SlabRunner(kind.dim, n, kind, world=world, rank=rank, ghost_sweeps=per,
-                       ghost=2 * per)
+                       ghost=2 * per, overlap=n >= 20)   # n >= 20: boundary / interior split
         r._pass = oracle_pass(r, name)
         r.init(7, 8, 0.8)
         r.sweep(sweeps)
