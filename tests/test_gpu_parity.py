@@ -360,3 +360,24 @@ def test_sweep_pass_windows_compose(name, n):
     assert _bits_equal(whole.cpu().numpy(), want)
     assert _bits_equal(parts.cpu().numpy(), want)
     assert int(status.item()) == 0
+
+
+@pytest.mark.parametrize("name,n,flags", [("fe9", 130, _native.SL_FLAG_STREAM), ("fe9", 64, 0),
+                                          ("fd5", 130, _native.SL_FLAG_STREAM), ("fd7", 34, 0),
+                                          ("fe27q1", 30, 0), ("fe27", 18, 0)])
+def test_nonfinite_raises_on_every_fused_kernel(name, n, flags):
+    """A non-finite interior value (Form D) or right-hand side surfaces as
+    NumericsError from the streaming, tile and Q1 kernels alike."""
+    kind = sl.get_stencil(name)
+    for where in ("u", "f"):
+        m = sl.make_mesh(kind.dim, n, seed=3)
+        sl.init_rhs(m, 4, 0.8)
+        c = (n // 2,) * kind.dim
+        if where == "u":
+            m.values[m.flat_index(c)] = np.inf
+        else:
+            f = m._rhs_host.copy()
+            f[m.flat_index(c)] = np.nan
+            m.set_rhs(f, 0.8)
+        with pytest.raises(sl.NumericsError):
+            sl.run_sweeps(m, kind, sl.CostModel(), 2, flags=flags)
