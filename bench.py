@@ -39,6 +39,9 @@ FALLBACK_HBM_GBS = 6650.0
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--exchange", choices=("nccl", "peer"), default="nccl",
+                    help="slab halo exchange (N > 1): NCCL send/recv after the pass, or stores of the "
+                         "boundary planes into the neighbours' ghost planes fused into the pass")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
@@ -291,10 +294,12 @@ def run_ours(args, wl, rank, world, local):
         # sweeps (5-sweep ghost rows, <2% redundant rows) so the host issues ~1.4 launches per
         # sweep; 3D slabs exchange every sweep (a deeper z ghost would cost 6-12% extra planes)
         sr = SlabRunner(wl.dim, wl.n, kind, world=world, rank=rank,
-                        ghost_sweeps=5 if wl.dim == 2 and wl.sweeps % 5 == 0 else 1, device=dev)
+                        ghost_sweeps=5 if wl.dim == 2 and wl.sweeps % 5 == 0 else 1, device=dev,
+                        exchange=args.exchange)
         sr.init(wl.seed, wl.seed + 1, wl.omega)
         total_updates, scaling = wl.updates, "strong"
-        parallelism = f"slabs x{world} (axis {'z' if wl.dim == 3 else 'y'}, ghost {sr.layout.ghost}, NCCL P2P)"
+        how = "NCCL P2P" if args.exchange == "nccl" else "peer stores fused into the pass"
+        parallelism = f"slabs x{world} (axis {'z' if wl.dim == 3 else 'y'}, ghost {sr.layout.ghost}, {how})"
         u_host = sr.u.cpu().pin_memory()
         f_host = sr.f.cpu().pin_memory()
         out_host = torch.empty_like(sr.owned()).cpu().pin_memory()

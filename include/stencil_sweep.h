@@ -117,6 +117,16 @@ SL_API int sl_sweep(const sl_grid *g, const sl_stencil *s, int32_t sweeps, uint3
 SL_API int sl_sweep_pass(const sl_grid *g, const sl_stencil *s, const double *src, double *dst,
                          int64_t zbegin, int64_t zend, int32_t *d_status, void *stream);
 
+/* sl_sweep_pass that also stores every owned value of slow-axis plane
+ * q <= dn_last at peer_dn + e and of plane q >= up_first at peer_up + e, where
+ * e is the value's element index in g's layout.  The slab runner passes the
+ * neighbouring ranks' slab buffers (peer memory over NVLink), offset so that
+ * e lands in their ghost planes: the halo exchange is fused into the pass and
+ * overlaps it store by store.  NULL peers = sl_sweep_pass.  16-byte aligned. */
+SL_API int sl_sweep_pass_peer(const sl_grid *g, const sl_stencil *s, const double *src, double *dst,
+                              int64_t zbegin, int64_t zend, double *peer_dn, int64_t dn_last,
+                              double *peer_up, int64_t up_first, int32_t *d_status, void *stream);
+
 /* One colour phase in place: one parallel_for pass of sweep_colouring
  * (strategies.py:374-393) / one colour of sweep_colouring_reference (:420-433). */
 SL_API int sl_colour_pass(const sl_grid *g, const sl_stencil *s, int32_t colour,

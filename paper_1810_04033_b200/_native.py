@@ -27,7 +27,7 @@ ABI_VERSION = 1
 EXPORTS = ("sl_abi_version", "sl_strerror", "sl_last_cuda_error", "sl_launch_count",
            "sl_workspace_bytes",
            "sl_sweep", "sl_colour_pass", "sl_update_cells", "sl_residual_max", "sl_ghost_depth",
-           "sl_sweep_cost", "sl_update_cells_cost", "sl_sweep_pass")
+           "sl_sweep_cost", "sl_update_cells_cost", "sl_sweep_pass", "sl_sweep_pass_peer")
 
 
 class NativeLibraryError(RuntimeError):
@@ -65,6 +65,10 @@ _SIGS = {
                                 ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p]),
     "sl_sweep_pass": (ctypes.c_int, [_P(SlGrid), _P(SlStencil), ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
+    "sl_sweep_pass_peer": (ctypes.c_int, [_P(SlGrid), _P(SlStencil), ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                          ctypes.c_void_p]),
     "sl_colour_pass": (ctypes.c_int, [_P(SlGrid), _P(SlStencil), ctypes.c_int32,
                                       ctypes.c_void_p, ctypes.c_void_p]),
     "sl_update_cells": (ctypes.c_int, [_P(SlGrid), _P(SlStencil), ctypes.c_void_p,

@@ -241,8 +241,9 @@ int sl_sweep(const sl_grid *g, const sl_stencil *s, int32_t sweeps, uint32_t fla
   return SL_OK;
 }
 
-int sl_sweep_pass(const sl_grid *g, const sl_stencil *s, const double *src, double *dst, int64_t zbegin,
-                  int64_t zend, int32_t *d_status, void *stream) {
+static int sweep_pass_impl(const sl_grid *g, const sl_stencil *s, const double *src, double *dst,
+                           int64_t zbegin, int64_t zend, double *pdn, int64_t dn_last, double *pup,
+                           int64_t up_first, int32_t *d_status, void *stream) {
   if (!g || !src || !dst || src == dst) return SL_E_INVAL;
   sl_grid gs = *g;
   gs.u = const_cast<double *>(src);
@@ -254,10 +255,27 @@ int sl_sweep_pass(const sl_grid *g, const sl_stencil *s, const double *src, doub
   if (empty_grid(p)) return SL_OK;
   p.zlo = (int32_t)zbegin;
   p.zhi = (int32_t)zend;
+  if ((pdn && ((uintptr_t)pdn & 15)) || (pup && ((uintptr_t)pup & 15))) return SL_E_INVAL;
+  p.pdn = pdn;
+  p.pup = pup;
+  p.dn_last = (int32_t)(dn_last < -1 ? -1 : (dn_last > p.zhi ? p.zhi : dn_last));
+  p.up_first = (int32_t)(up_first < 0 ? 0 : (up_first > (int64_t)1 << 30 ? (int64_t)1 << 30 : up_first));
   int handled = 0;
   rc = cuda_status(launch_one_pass(key, p, src, dst, (cudaStream_t)stream, &handled));
   if (rc != SL_OK) return rc;
   return handled ? SL_OK : SL_E_UNSUPPORTED;
+}
+
+int sl_sweep_pass(const sl_grid *g, const sl_stencil *s, const double *src, double *dst, int64_t zbegin,
+                  int64_t zend, int32_t *d_status, void *stream) {
+  return sweep_pass_impl(g, s, src, dst, zbegin, zend, nullptr, -1, nullptr, 0, d_status, stream);
+}
+
+int sl_sweep_pass_peer(const sl_grid *g, const sl_stencil *s, const double *src, double *dst,
+                       int64_t zbegin, int64_t zend, double *peer_dn, int64_t dn_last, double *peer_up,
+                       int64_t up_first, int32_t *d_status, void *stream) {
+  return sweep_pass_impl(g, s, src, dst, zbegin, zend, peer_dn, dn_last, peer_up, up_first, d_status,
+                         stream);
 }
 
 int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats, int64_t count,

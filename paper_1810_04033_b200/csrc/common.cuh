@@ -84,7 +84,22 @@ struct Params {
   double wc, rwc, omega;
   int64_t delta[26];  // flat deltas (update_cells / residual)
   int32_t zlo, zhi;   // fused passes: output planes [zlo, zhi) of the slowest axis (z; y in 2D)
+  // slab runner, peer exchange: owned planes <= dn_last also go to pdn + e, planes >= up_first
+  // to pup + e (e = the element's index in this grid; the pointers are pre-offset so that e
+  // lands in the neighbour's ghost planes, in its memory over NVLink)
+  double *pdn, *pup;
+  int32_t dn_last, up_first;
 };
+
+__device__ __forceinline__ void stg_pair_any(double *p, double a, double b) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(a), "d"(b) : "memory");
+}
+
+// the peer copies of an owned value pair stored at element e of slow-axis plane `plane`
+__device__ __forceinline__ void stg_pair_peers(const Params &p, int plane, int64_t e, double a, double b) {
+  if (p.pdn && plane <= p.dn_last) stg_pair_any(p.pdn + e, a, b);
+  if (p.pup && plane >= p.up_first) stg_pair_any(p.pup + e, a, b);
+}
 
 template <int FORM, bool UNIT, int DIV>
 __device__ __forceinline__ double div_wc(double a, const Params &p) {

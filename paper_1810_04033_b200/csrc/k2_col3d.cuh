@@ -270,7 +270,11 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
             if (pz >= z0 && pz < z1) {
 #pragma unroll
               for (int a = 0; a < G::RT; ++a)
-                if ((own >> a) & 1u) stg_pair(dst + (int64_t)pz * p.sz + rowoff[a], U[a][SM2][0], U[a][SM2][1]);
+                if ((own >> a) & 1u) {
+                  const int64_t e = (int64_t)pz * p.sz + rowoff[a];
+                  stg_pair(dst + e, U[a][SM2][0], U[a][SM2][1]);
+                  stg_pair_peers(p, pz, e, U[a][SM2][0], U[a][SM2][1]);
+                }
             }
             __syncthreads();
             // slots of planes t-3 (u) / t-4 (f) are free: refill them D planes ahead

@@ -299,7 +299,11 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
       double *pb = dst + (int64_t)gz_out * p.sz;
 #pragma unroll
       for (int k = 0; k < G::LPT; ++k)
-        if ((ownm >> k) & 1) stg2(pb + goff[k], sm[sout + soff[k]], sm[sout + soff[k] + G::HW]);
+        if ((ownm >> k) & 1) {
+          stg2(pb + goff[k], sm[sout + soff[k]], sm[sout + soff[k] + G::HW]);
+          stg_pair_peers(p, gz_out, (int64_t)gz_out * p.sz + goff[k], sm[sout + soff[k]],
+                         sm[sout + soff[k] + G::HW]);
+        }
     }
     {  // rotate: the slot of plane t-LAGMAX-1 becomes the slot of plane t+2
       const int tmp = so[G::W - 1];

@@ -354,7 +354,10 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
       double *dp = dthr + (int64_t)po * sz;
 #pragma unroll
       for (int a = 0; a < RT; ++a)
-        if ((ownbits >> a) & 1u) stg_pair(dp + a * sy32, U[a][E][0], U[a][E][1]);
+        if ((ownbits >> a) & 1u) {
+          stg_pair(dp + a * sy32, U[a][E][0], U[a][E][1]);
+          stg_pair_peers(p, po, (int64_t)po * sz + rowoff0 + a * sy32, U[a][E][0], U[a][E][1]);
+        }
     }
   };
 

@@ -328,6 +328,7 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                            (in_y && gx + 2 * k + 1 <= nx &&
                             ((unsigned)__double2hiint(b) & 0x7ff00000u) == 0x7ff00000u);
                     stg_pair(dst + (int64_t)row * p.sy + gx + 2 * k, a, b);
+                    stg_pair_peers(p, row, (int64_t)row * p.sy + gx + 2 * k, a, b);
                   }
                 }
               }

@@ -104,14 +104,19 @@ class SlabRunner:
 
     def __init__(self, dim: int, n: int, kind: StencilKind, world: int = 1, rank: int = 0,
                  ghost_sweeps: int = 1, device=None, group=None, compute=None, ghost: int = None,
-                 overlap: bool = False):
+                 overlap: bool = False, exchange: str = "nccl"):
         import torch
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"exchange must be 'nccl' or 'peer', not {exchange!r}")
         if kind.dim != dim:
             raise ValueError(f"{kind.name} is {kind.dim}D, not {dim}D")
         self.dim, self.n, self.kind = dim, n, kind
         self.world, self.rank, self.group = world, rank, group
         self.ghost_sweeps = ghost_sweeps
         self.overlap = overlap   # boundary passes first, exchange during the interior pass
+        # "peer": the last pass of a round stores the boundary planes straight into the
+        # neighbours' ghost planes (peer memory); a stream-ordered barrier ends the round
+        self.exchange_mode = exchange
         g = ghost if ghost is not None else ghost_depth(kind, ghost_sweeps)
         self.layout = SlabLayout(n, world, rank, g)
         if world > 1:
@@ -120,8 +125,18 @@ class SlabRunner:
         nl = self.layout.local_interior
         self.shape = (nl + 2, s) if dim == 2 else (nl + 2, s, s)
         self.device = torch.device(device) if device is not None else torch.device("cpu")
-        self.u = torch.zeros(self.shape, dtype=torch.float64, device=self.device)
-        self._u2 = torch.zeros_like(self.u)   # the other buffer of the pass ping-pong
+        self._symm = None
+        import torch.distributed as dist
+        if (exchange == "peer" and world > 1 and self.device.type == "cuda" and dist.is_available()
+                and dist.is_initialized()):
+            bufs = self._symmetric_buffers()     # one process per GPU: peer memory over NVLink
+        else:
+            bufs = (torch.zeros(self.shape, dtype=torch.float64, device=self.device),
+                    torch.zeros(self.shape, dtype=torch.float64, device=self.device))
+        self._bufs = bufs                     # fixed roles: buffer 0 / 1 of the ping-pong
+        self._cur = 0                         # index of the buffer holding the current state
+        self.u, self._u2 = bufs               # the other buffer of the pass ping-pong
+        self._peers = None                    # per dst buffer: (pdn, pup) element pointers
         self.f = None
         self.omega = None
         self._pass = compute or self._gpu_pass   # (src, dst, z0, z1): one sweep into dst planes [z0, z1)
@@ -257,6 +272,84 @@ class SlabRunner:
 
     def _swap(self):
         self.u, self._u2 = self._u2, self.u
+        self._cur ^= 1
+
+    # -- fused peer exchange ------------------------------------------------------
+
+    def _symmetric_buffers(self):
+        """Both slab buffers in symmetric memory (same size on every rank),
+        so each rank can address its neighbours' buffers over NVLink."""
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        nl_max = max(SlabLayout(self.n, self.world, r, self.layout.ghost).local_interior
+                     for r in range(self.world))
+        full = (nl_max + 2,) + self.shape[1:]
+        group = self.group if self.group is not None else dist.group.WORLD
+        bufs, hdls = [], []
+        for _ in range(2):
+            t = symm_mem.empty(*full, dtype=torch.float64, device=self.device)
+            hdls.append(symm_mem.rendezvous(t, group))
+            t.zero_()
+            bufs.append(t[:self.shape[0]])
+        self._symm = hdls
+        ranks = dist.get_process_group_ranks(group)
+        lo_of = [SlabLayout(self.n, self.world, r, self.layout.ghost).lo for r in range(self.world)]
+        pe = self.plane_elems() * 8
+        peers = []
+        for d in range(2):
+            ptrs = hdls[d].buffer_ptrs
+            dn = ptrs[self.rank - 1] + (self.layout.lo - lo_of[self.rank - 1]) * pe if self.rank > 0 else None
+            up = (ptrs[self.rank + 1] + (self.layout.lo - lo_of[self.rank + 1]) * pe
+                  if self.rank < self.world - 1 else None)
+            peers.append((dn, up))
+        del ranks
+        self._peer_init = peers
+        hdls[0].barrier(channel=0)
+        return tuple(bufs)
+
+    def connect_peers(self, lower=None, upper=None):
+        """Peer exchange between runners of one process (tests; one device):
+        the neighbours' buffers stand in for peer memory."""
+        pe = self.plane_elems() * 8
+        peers = []
+        for d in range(2):
+            dn = (lower._bufs[d].data_ptr() + (self.layout.lo - lower.layout.lo) * pe) if lower else None
+            up = (upper._bufs[d].data_ptr() + (self.layout.lo - upper.layout.lo) * pe) if upper else None
+            peers.append((dn, up))
+        self._peers = peers
+
+    def _gpu_pass_peer(self, src, dst, z0: int, z1: int, peers):
+        import torch
+        lib = _native.require_cuda()
+        g, st = self._descriptors()
+        if self._status is None:
+            self._status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        L, G = self.layout, self.layout.ghost
+        a, b = L.a - L.lo, L.b - L.lo
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        rc = lib.sl_sweep_pass_peer(ctypes.byref(g), ctypes.byref(st), src.data_ptr(), dst.data_ptr(),
+                                    z0, z1, peers[0], a + G, peers[1], b - G,
+                                    self._status.data_ptr(), stream)
+        _native.check(rc, "slab peer pass")
+
+    def round_begin(self, k: int):
+        """The k-1 redundant sweeps of a round over the whole local slab."""
+        whole = self.shape[0]
+        for _ in range(k - 1):
+            self._pass(self.u, self._u2, 0, whole)
+            self._swap()
+
+    def round_end_peer(self):
+        """Last sweep of a round in peer mode: one pass over the owned planes
+        whose boundary-plane stores also land in the neighbours' ghost planes."""
+        L = self.layout
+        if self._peers is None:
+            if self._symm is None:
+                raise RuntimeError("peer exchange needs connect_peers() or symmetric buffers")
+            self._peers = self._peer_init
+        self._gpu_pass_peer(self.u, self._u2, L.a - L.lo, L.b - L.lo + 1, self._peers[self._cur ^ 1])
+        self._swap()
 
     def compute_round(self, k: int, exchange: bool = False):
         """k sweeps of the slab (k <= ghost_sweeps); with `exchange`, the
@@ -269,10 +362,16 @@ class SlabRunner:
             if exchange:
                 self.exchange()
             return
-        whole = self.shape[0]
-        for _ in range(k - 1):   # redundant sweeps of the whole local slab
-            self._pass(self.u, self._u2, 0, whole)
-            self._swap()
+        self.round_begin(k)
+        if self.exchange_mode == "peer" and self.world > 1:
+            if k > 1 and self._symm is not None:
+                # neighbours' redundant passes write whole buffers, ghost planes included:
+                # they must be done before this rank's stores reach those planes
+                self._symm[0].barrier(channel=0)
+            self.round_end_peer()
+            if exchange and self._symm is not None:
+                self._symm[0].barrier(channel=0)   # every rank's stores are in before anyone reads
+            return
         a, b = L.a - L.lo, L.b - L.lo          # owned planes, local indices
         if self.world == 1 or not self.overlap or b - a + 1 <= 2 * (G + 1):
             self._pass(self.u, self._u2, a, b + 1)

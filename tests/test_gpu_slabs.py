@@ -66,3 +66,43 @@ def test_single_rank_slab_runner():
     want = R.init_u(3, 24, 7)
     coracle.sweep(want, "fd7", 3, f=R.init_f(3, 24, 8), omega=0.8, form="D")
     assert np.array_equal(r.gather().view(np.int64), want.view(np.int64))
+
+
+@pytest.mark.parametrize("name,n,sweeps,world,per", [
+    ("fd7", 40, 5, 2, 1), ("fd7", 38, 4, 3, 2), ("fe27q1", 30, 3, 2, 1), ("fe27q1", 36, 2, 3, 1),
+    ("fe9", 130, 4, 3, 1), ("fe9", 98, 5, 2, 2), ("fd5", 66, 6, 4, 2), ("fe27", 24, 2, 2, 1)])
+def test_emulated_peer_exchange_equals_single_domain(name, n, sweeps, world, per):
+    """The fused exchange: each rank's last pass of a round stores its
+    boundary planes straight into the neighbours' ghost planes (here the
+    neighbours' buffers on the same device stand in for peer memory)."""
+    kind = sl.get_stencil(name)
+    dim = kind.dim
+    rs = [SlabRunner(dim, n, kind, world=world, rank=r, ghost_sweeps=per, device="cuda", exchange="peer")
+          for r in range(world)]
+    for i, r in enumerate(rs):
+        r.init(7, 8, 0.8)
+        r.connect_peers(rs[i - 1] if i > 0 else None, rs[i + 1] if i + 1 < world else None)
+    left = sweeps
+    while left > 0:
+        k = min(per, left)
+        for r in rs:            # all ranks' redundant sweeps, then all ranks' fused last passes
+            r.round_begin(k)
+        for r in rs:
+            r.round_end_peer()
+        left -= k
+    for r in rs:
+        r.check_status()
+    want = R.init_u(dim, n, 7)
+    coracle.sweep(want, name, sweeps, f=R.init_f(dim, n, 8), omega=0.8, form="D")
+    out = np.zeros((n + 2,) * dim)
+    for i, r in enumerate(rs):
+        L = r.layout
+        lo = 0 if i == 0 else L.a
+        hi = n + 1 if i == world - 1 else L.b
+        out[lo:hi + 1] = r.u[lo - L.lo:hi + 1 - L.lo].cpu().numpy()
+        # the ghost planes a neighbour stored are exactly its owned planes
+        if i > 0:
+            Lp = rs[i - 1].layout
+            assert np.array_equal(r.u[0:L.a - L.lo].cpu().numpy(),
+                                  rs[i - 1].u[L.lo - Lp.lo:L.a - Lp.lo].cpu().numpy())
+    assert np.array_equal(out.view(np.int64), want.view(np.int64))
