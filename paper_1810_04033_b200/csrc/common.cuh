@@ -96,9 +96,14 @@ __device__ __forceinline__ void stg_pair_any(double *p, double a, double b) {
 }
 
 // the peer copies of an owned value pair stored at element e of slow-axis plane `plane`
+// (compiled in only for the peer-exchange instantiations: the checks cost the
+// plain passes up to 10 %)
+template <bool PEER>
 __device__ __forceinline__ void stg_pair_peers(const Params &p, int plane, int64_t e, double a, double b) {
-  if (p.pdn && plane <= p.dn_last) stg_pair_any(p.pdn + e, a, b);
-  if (p.pup && plane >= p.up_first) stg_pair_any(p.pup + e, a, b);
+  if constexpr (PEER) {
+    if (p.pdn && plane <= p.dn_last) stg_pair_any(p.pdn + e, a, b);
+    if (p.pup && plane >= p.up_first) stg_pair_any(p.pup + e, a, b);
+  }
 }
 
 template <int FORM, bool UNIT, int DIV>

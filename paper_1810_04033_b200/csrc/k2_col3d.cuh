@@ -53,7 +53,7 @@ struct Col3Geo {
 };
 
 // Exact division out of line (rare fallback of the Markstein fast path).
-__device__ __noinline__ double col3_div_exact(double a, double b) { return __ddiv_rn(a, b); }
+static __device__ __noinline__ double col3_div_exact(double a, double b) { return __ddiv_rn(a, b); }
 
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int x, int y, int z,
                                             uint32_t mbar) {
@@ -81,7 +81,7 @@ __device__ __forceinline__ void mbar_wait3(uint32_t addr, uint32_t parity) {
       : "memory");
 }
 
-template <int FORM, bool UNIT, int DIV>
+template <int FORM, bool UNIT, int DIV, bool PEER = false>
 __global__ void __launch_bounds__(Col3Geo::NT, 1)
 k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_constant__ CUtensorMap tmf,
              double *__restrict__ dst, int64_t ntx, int64_t nty, int64_t nzc) {
@@ -273,7 +273,7 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
                 if ((own >> a) & 1u) {
                   const int64_t e = (int64_t)pz * p.sz + rowoff[a];
                   stg_pair(dst + e, U[a][SM2][0], U[a][SM2][1]);
-                  stg_pair_peers(p, pz, e, U[a][SM2][0], U[a][SM2][1]);
+                  stg_pair_peers<PEER>(p, pz, e, U[a][SM2][0], U[a][SM2][1]);
                 }
             }
             __syncthreads();

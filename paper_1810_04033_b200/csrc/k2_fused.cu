@@ -165,7 +165,7 @@ __host__ __device__ constexpr int x_parity(int colours, int c, int qy, int qz) {
 // ---------------------------------------------------------------------------
 // 3D: z-streaming over (TX x TY) tiles
 
-template <int S, int FORM, bool UNIT, int DIV, int M>
+template <int S, int FORM, bool UNIT, int DIV, int M, bool PEER = false>
 __global__ void __launch_bounds__(Geo3<S, M>::NT, Geo3<S, M>::MINB)
 k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, Tiles tl) {
   using G = Geo3<S, M>;
@@ -301,7 +301,7 @@ k2_stream3d(Params p, const double *__restrict__ src, double *__restrict__ dst, 
       for (int k = 0; k < G::LPT; ++k)
         if ((ownm >> k) & 1) {
           stg2(pb + goff[k], sm[sout + soff[k]], sm[sout + soff[k] + G::HW]);
-          stg_pair_peers(p, gz_out, (int64_t)gz_out * p.sz + goff[k], sm[sout + soff[k]],
+          stg_pair_peers<PEER>(p, gz_out, (int64_t)gz_out * p.sz + goff[k], sm[sout + soff[k]],
                          sm[sout + soff[k] + G::HW]);
         }
     }
@@ -363,11 +363,13 @@ static bool fused_supported(const KernelKey &key, const Params &p) {
   return true;
 }
 
+#ifndef SL_PEER_TU
 size_t fused_workspace_bytes(const KernelKey &key, const Params &p) {
   if (!fused_supported(key, p)) return 0;
   const int64_t elems = (p.nx + 2) * (p.ny + 2) * (shape_dim(key.shape) == 3 ? (p.nz + 2) : 1);
   return (size_t)elems * sizeof(double);
 }
+#endif
 
 // Chunks along the streaming axis: balance wave quantisation against the
 // per-chunk warm-up/drain cost (`extra` steps per chunk).
@@ -426,10 +428,10 @@ static cudaError_t make_tmap3(CUtensorMap *map, const double *base, const Params
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int S, int FORM, bool UNIT, int DIV, int M>
+template <int S, int FORM, bool UNIT, int DIV, int M, bool PEER = false>
 static cudaError_t launch_stream3d(const Params &p, const double *src, double *dst, cudaStream_t st) {
     using G = Geo3<S, M>;
-    auto kern = k2_stream3d<S, FORM, UNIT, DIV, M>;
+    auto kern = k2_stream3d<S, FORM, UNIT, DIV, M, PEER>;
     static thread_local int64_t slots = 0;
     if (!slots) {
       cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
@@ -463,11 +465,11 @@ static bool q1_two_weights(const Params &p) {
   return true;
 }
 
-template <int S, int FORM, bool UNIT, int DIV, int M>
+template <int S, int FORM, bool UNIT, int DIV, int M, bool PEER = false>
 static cudaError_t launch_pass(const Params &p, const double *src, double *dst, cudaStream_t st) {
   if constexpr (S == FD7 && M == 1) {
     using G = Col3Geo;
-    auto kern = k2_col3d_fd7<FORM, UNIT, DIV>;
+    auto kern = k2_col3d_fd7<FORM, UNIT, DIV, PEER>;
     static thread_local int64_t slots = 0;
     if (!slots) {
       cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
@@ -484,9 +486,9 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     note_launch();
     return cudaGetLastError();
   } else if constexpr (S == Q1 && M == 1) {
-    if (!q1_two_weights(p)) return launch_stream3d<S, FORM, UNIT, DIV, M>(p, src, dst, st);
+    if (!q1_two_weights(p)) return launch_stream3d<S, FORM, UNIT, DIV, M, PEER>(p, src, dst, st);
     using G = Q1Geo;
-    auto kern = k2_q1col<FORM, UNIT, DIV>;
+    auto kern = k2_q1col<FORM, UNIT, DIV, PEER>;
     static thread_local int64_t slots = 0;
     if (!slots) {
       cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
@@ -502,7 +504,7 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     note_launch();
     return cudaGetLastError();
   } else if constexpr (shape_dim(S) == 3) {
-    return launch_stream3d<S, FORM, UNIT, DIV, M>(p, src, dst, st);
+    return launch_stream3d<S, FORM, UNIT, DIV, M, PEER>(p, src, dst, st);
   } else {
     using G = GeoS2<S, M>;
     auto run = [&](auto kern) -> cudaError_t {
@@ -522,9 +524,10 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     };
     cudaError_t e;
     if constexpr (S == FE9 && !UNIT)
-      e = equal_weights(p, S) ? run(k2_strip2d<S, FORM, UNIT, DIV, M, true>) : run(k2_strip2d<S, FORM, UNIT, DIV, M>);
+      e = equal_weights(p, S) ? run(k2_strip2d<S, FORM, UNIT, DIV, M, true, PEER>)
+                              : run(k2_strip2d<S, FORM, UNIT, DIV, M, false, PEER>);
     else
-      e = run(k2_strip2d<S, FORM, UNIT, DIV, M>);
+      e = run(k2_strip2d<S, FORM, UNIT, DIV, M, false, PEER>);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
@@ -587,6 +590,15 @@ static cudaError_t launch_block2d(const Params &p, const double *src, double *ds
   return cudaGetLastError();
 }
 
+#ifdef SL_PEER_TU
+// the peer-exchange instantiations (own translation unit: k2_peer.cu)
+cudaError_t launch_one_pass_peer(const KernelKey &key, const Params &p, const double *src, double *dst,
+                                 cudaStream_t st) {
+  return dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
+    return launch_pass<S, F, U, D, 1, true>(p, src, dst, st);
+  });
+}
+#else
 cudaError_t launch_one_pass(const KernelKey &key, const Params &p, const double *src, double *dst,
                             cudaStream_t st, int *handled) {
   *handled = 0;
@@ -594,6 +606,7 @@ cudaError_t launch_one_pass(const KernelKey &key, const Params &p, const double 
   if (((uintptr_t)src & 15) || ((uintptr_t)dst & 15)) return cudaSuccess;
   *handled = 1;
   if (p.zhi <= p.zlo) return cudaSuccess;
+  if (p.pdn || p.pup) return launch_one_pass_peer(key, p, src, dst, st);
   return dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
     return launch_pass<S, F, U, D, 1>(p, src, const_cast<double *>(dst), st);
   });
@@ -661,5 +674,7 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
   }
   return e;
 }
+
+#endif  // SL_PEER_TU
 
 }  // namespace sl

@@ -18,4 +18,8 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
 cudaError_t launch_one_pass(const KernelKey &key, const Params &p, const double *src, double *dst,
                             cudaStream_t st, int *handled);
 
+// launch_one_pass with the peer stores of p.pdn / p.pup compiled in (k2_peer.cu)
+cudaError_t launch_one_pass_peer(const KernelKey &key, const Params &p, const double *src, double *dst,
+                                 cudaStream_t st);
+
 }  // namespace sl

@@ -27,8 +27,10 @@
 // u planes arrive by TMA (64 x 49 x 1 boxes, zero-filled out of range) into
 // 8 smem slots, up to six planes ahead.  The loop is unrolled by two pair
 // steps (one ring turn), so ring indices are compile-time; slot offsets and
-// mbarrier parities are cheap runtime values.  Out-of-range groups and ghost
-// points are computed and masked (no branches around the shuffles); the exact
+// mbarrier parities are cheap runtime values.  A group with no used point in
+// a warp (out-of-range planes, top/bottom warps of the later groups) is
+// skipped by that warp; other ghost points are computed and masked (no
+// branches around the shuffles); the exact
 // division fallback runs out of line, per warp, only when a used lane's
 // operand leaves the fast range.
 #pragma once
@@ -40,7 +42,7 @@ namespace sl {
 
 // Exact division out of line: the rare fallback of the Markstein fast path
 // must not bloat the unrolled loop (instruction-cache pressure).
-__device__ __noinline__ double q1_div_exact(double a, double b) { return __ddiv_rn(a, b); }
+static __device__ __noinline__ double q1_div_exact(double a, double b) { return __ddiv_rn(a, b); }
 
 struct Q1Geo {
   static constexpr FPlan P = make_plan(Q1, 8, 1, false);
@@ -68,7 +70,7 @@ constexpr bool q1_plan_ok() {
 }
 static_assert(q1_plan_ok(), "unexpected plan");
 
-template <int FORM, bool UNIT, int DIV>
+template <int FORM, bool UNIT, int DIV, bool PEER = false>
 __global__ void __launch_bounds__(Q1Geo::NT, 1)
 k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__ dst, int64_t ntx,
          int64_t nty, int64_t nzc) {
@@ -152,6 +154,16 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
       }
     }
   }
+  // groups with no used point in this warp (its rows lie outside the group's
+  // need region: top/bottom warps of the tile for the later colour groups)
+  // are skipped whole; a masked update leaves the ring and its slot as they are
+  unsigned gmask = 0;
+#pragma unroll
+  for (int gi = 0; gi < 4; ++gi)
+    gmask |= __any_sync(0xffffffffu, (okbits >> (4 * gi)) & 0xFu) ? (1u << gi) : 0u;
+#ifdef Q1_NOSKIP
+  gmask = 0xFu;
+#endif
   // owned output rows (the tiles partition [0, S) in x and y)
   const bool colown = 2 * lane >= G::GX && 2 * lane < G::GX + TXo;
   unsigned ownbits = 0, fokbits = 0;
@@ -232,6 +244,7 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
     constexpr int NZJ = cmax(P.need[2 * GI][2], P.need[2 * GI + 1][2]);
     const int pz = pp - LAGG;
     const bool okz = pz >= 1 && pz <= nz && pz >= z0 - NZJ && pz < z1 + NZJ;
+    if (!okz || !((gmask >> GI) & 1u)) return;   // warp-uniform
     double acc[H][2];
 #pragma unroll
     for (int h = 0; h < H; ++h)
@@ -356,7 +369,7 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
       for (int a = 0; a < RT; ++a)
         if ((ownbits >> a) & 1u) {
           stg_pair(dp + a * sy32, U[a][E][0], U[a][E][1]);
-          stg_pair_peers(p, po, (int64_t)po * sz + rowoff0 + a * sy32, U[a][E][0], U[a][E][1]);
+          stg_pair_peers<PEER>(p, po, (int64_t)po * sz + rowoff0 + a * sy32, U[a][E][0], U[a][E][1]);
         }
     }
   };

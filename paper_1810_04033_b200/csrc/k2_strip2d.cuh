@@ -93,13 +93,13 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
 }
 
 // Exact division out of line (rare fallback of the Markstein fast path).
-__device__ __noinline__ double strip_div_exact(double a, double b) { return __ddiv_rn(a, b); }
+static __device__ __noinline__ double strip_div_exact(double a, double b) { return __ddiv_rn(a, b); }
 
 // EQW: every neighbour weight equal (FE9: -1/3; host-checked).  Then each
 // value's product w * u is rounded once per phase and shared by the lane's
 // points and, through the shuffle, by the adjacent lane — the same rounded
 // terms, added in the same canonical order.
-template <int S, int FORM, bool UNIT, int DIV, int M, bool EQW = false>
+template <int S, int FORM, bool UNIT, int DIV, int M, bool EQW = false, bool PEER = false>
 __global__ void __launch_bounds__(32 * GeoS2<S, M>::WPB)
 k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, int64_t nstrip,
            int64_t nchunk) {
@@ -328,7 +328,7 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
                            (in_y && gx + 2 * k + 1 <= nx &&
                             ((unsigned)__double2hiint(b) & 0x7ff00000u) == 0x7ff00000u);
                     stg_pair(dst + (int64_t)row * p.sy + gx + 2 * k, a, b);
-                    stg_pair_peers(p, row, (int64_t)row * p.sy + gx + 2 * k, a, b);
+                    stg_pair_peers<PEER>(p, row, (int64_t)row * p.sy + gx + 2 * k, a, b);
                   }
                 }
               }
