@@ -93,13 +93,20 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except Exception:
             self.proc = None
-        time.sleep(0.15)
+            return
+        # nvidia-smi can take seconds to start on a fresh box: wait for its
+        # first sample so the timed region is covered, then keep only what
+        # follows
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 15 and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.mark = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -108,7 +115,11 @@ class ClockSampler:
     def stop(self):
         if self.proc is None:
             return None
-        time.sleep(0.15)
+        # a short timed region still gets at least two samples (the second
+        # may land just after it, at the clocks the load left)
+        t0 = time.time()
+        while len(self.lines) - getattr(self, "mark", 0) < 2 and time.time() - t0 < 2:
+            time.sleep(0.01)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -116,7 +127,7 @@ class ClockSampler:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "mark", 0):]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -356,11 +367,11 @@ def run_ours(args, wl, rank, world, local):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()   # before the barrier: its start-up must not delay rank 0's timed region
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    if clocks:
-        clocks.start()
     launches0 = lib.sl_launch_count()
     for i in range(args.steps):
         if flush_buf is not None:

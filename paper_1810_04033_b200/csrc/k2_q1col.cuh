@@ -52,7 +52,10 @@ struct Q1Geo {
   static constexpr int TX = PX - 2 * GX, TY = PY - 2 * GY;
   static constexpr int S = 8;                             // smem slots
   static constexpr int RR = 4;                            // ring entries (planes p-2 .. p live)
-  static constexpr int RT = 4;                            // tile rows per thread
+#ifndef Q1_RT
+#define Q1_RT 4
+#endif
+  static constexpr int RT = Q1_RT;                        // tile rows per thread
   static constexpr int NT = 32 * PY / RT;                 // 384
   static constexpr int LAGMAX = 1;
   static constexpr int SLOTE = PX * BOXY;
