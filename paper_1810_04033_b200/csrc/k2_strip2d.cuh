@@ -39,12 +39,15 @@ struct GeoS2 {
 #ifndef STRIP_WPB
 #define STRIP_WPB 2
 #endif
+#ifndef STRIP_NS
+#define STRIP_NS 8
+#endif
   static constexpr int NP = STRIP_NP;                  // column pairs per lane
   static constexpr int WS = 64 * NP;                   // strip width (columns)
   static constexpr int TX = WS - 2 * GX;
   static constexpr int NRR0 = LAGMAX + 3;             // register ring: rows t-LAGMAX-1 .. t+1
   static constexpr int NRR = NRR0 <= 2 ? 2 : (NRR0 <= 4 ? 4 : 8);
-  static constexpr int NS = 8;                         // smem ring slots (rows in flight)
+  static constexpr int NS = STRIP_NS;                  // smem ring slots (rows in flight)
   static constexpr int U = NRR > NS ? NRR : NS;        // unroll: multiple of both (powers of 2)
   static constexpr int WPB = STRIP_WPB;                // warps per block
   static constexpr int ROWB = WS * 8;                  // bytes of one array's row segment
