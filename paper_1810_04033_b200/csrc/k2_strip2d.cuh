@@ -40,7 +40,7 @@ struct GeoS2 {
 #define STRIP_WPB 2
 #endif
 #ifndef STRIP_NS
-#define STRIP_NS 8
+#define STRIP_NS 4
 #endif
   static constexpr int NP = STRIP_NP;                  // column pairs per lane
   static constexpr int WS = 64 * NP;                   // strip width (columns)
