@@ -4,8 +4,9 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
 A step is one pass of the hot path over one batch: the `sweeps` colour-ordered
-sweeps of BASELINE.json config C (default 2: FE9 8194^2, 4 colours, 50
-sweeps), run through the public API `run_sweeps` (one C-ABI sl_sweep call).
+sweeps of BASELINE.json config C (default 4, the largest single-GPU config:
+FE27-Q1 1026^3, 8 colours, 10 sweeps), run through the public API
+`run_sweeps` (one C-ABI sl_sweep call).
 Protocol mirrors the reference bench (bench.py:206-230): seeded init, W
 untimed warm-up steps, K timed steps, CUDA events on the launching stream;
 with N>1 (torchrun) the per-rank time is max-reduced.  Rank 0 prints ONE
@@ -44,7 +45,7 @@ def parse_args():
                          "boundary planes into the neighbours' ghost planes fused into the pass")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=4, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -161,25 +162,53 @@ def workload_config(wl, world, extra=None):
     return cfg
 
 
-def cpu_baseline(wl, budget_s=12.0):
-    """Time the C restatement (oracle/, all host threads) on a bounded sample."""
-    import numpy as np
-    from oracle import coracle
-    from oracle import restate as R
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    threads = coracle.max_threads()
-    n = wl.n
-    note = "full grid"
-    if wl.dim == 3 and n > 512:
-        n = 512
-        note = "n=512 sub-grid (full 1026^3 u+f would need 17 GB host RAM)"
+
+def host_ram_free():
+    try:
+        import psutil
+        return psutil.virtual_memory().available
+    except Exception:
+        return 0
+
+
+def cpu_grid(wl):
+    """Interior extent the CPU legs run: the full grid when the host can hold
+    u and f (1026^3: 17.3 GB) with margin, else an n=512 sub-grid (said so)."""
+    if wl.dim == 3 and wl.n > 512:
+        need = 2 * wl.grid_elems * 8
+        if host_ram_free() < 1.5 * need + (4 << 30):
+            return 512, f"n=512 sub-grid of the {wl.side}^3 config (host RAM < 1.5 x {need / 1e9:.1f} GB)"
+    return wl.n, "full grid"
+
+
+def cpu_inputs(wl, n):
+    from oracle import restate as R
     if wl.batch > 1:
         u, f = R.init_patches(min(wl.batch, 4096), wl.n, wl.seed)
-        note = f"{u.shape[0]} of {wl.batch} patches"
-    else:
-        u = R.init_u(wl.dim, n, wl.seed)
-        f = R.init_f(wl.dim, n, wl.seed + 1)
-    pts = u.size // (n + 2) ** wl.dim * n ** wl.dim
+        return u, f, u.shape[0] * wl.n ** 2, f"{u.shape[0]} of {wl.batch} patches"
+    u = R.init_u(wl.dim, n, wl.seed)
+    f = R.init_f(wl.dim, n, wl.seed + 1)
+    return u, f, n ** wl.dim, None
+
+
+def cpu_baseline(wl, budget_s=12.0):
+    """Time the C restatement (oracle/, all host threads) on a bounded sample."""
+    from oracle import coracle
+
+    threads = coracle.max_threads()
+    n, note = cpu_grid(wl)
+    u, f, pts, pnote = cpu_inputs(wl, n)
+    note = pnote or note
     t0 = time.perf_counter()
     coracle.sweep(u, wl.stencil, 1, f=f, omega=wl.omega, form="D", threads=threads)
     t1 = time.perf_counter()
@@ -190,10 +219,9 @@ def cpu_baseline(wl, budget_s=12.0):
         coracle.sweep(u, wl.stencil, more, f=f, omega=wl.omega, form="D", threads=threads)
         sweeps += more
     t2 = time.perf_counter()
-    del np
     return {"value": pts * sweeps / (t2 - t0) / 1e9, "unit": UNIT, "cores": threads,
-            "kind": "port",
-            "sample": f"{sweeps} sweep(s) of {wl.stencil} form D on the {note}, "
+            "kind": "port", "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+            "sample": f"{sweeps} of {wl.sweeps} sweep(s) of {wl.stencil} form D on the {note}, "
                       f"C restatement (oracle/sweep_oracle.c), {threads} pthreads"}
 
 
@@ -201,24 +229,12 @@ def run_reference(args, wl, rank, world):
     """The reference algorithm on the host cores (C port, all threads)."""
     if rank != 0:
         return
-    import numpy as np
     from oracle import coracle
-    from oracle import restate as R
 
     threads = coracle.max_threads()
-    n = wl.n
-    note = f"{wl.stencil} full grid"
-    if wl.dim == 3 and n > 512:
-        n = 512
-        note = f"{wl.stencil} n=512 sub-grid of the 1026^3 config"
-    if wl.batch > 1:
-        u, f = R.init_patches(min(wl.batch, 4096), wl.n, wl.seed)
-        note = f"{u.shape[0]} of {wl.batch} patches"
-        pts = u.shape[0] * wl.n ** 2
-    else:
-        u = R.init_u(wl.dim, n, wl.seed)
-        f = R.init_f(wl.dim, n, wl.seed + 1)
-        pts = n ** wl.dim
+    n, note = cpu_grid(wl)
+    u, f, pts, pnote = cpu_inputs(wl, n)
+    note = pnote or f"{wl.stencil} {note}"
     # one step = a bounded sample: as many sweeps as fit ~4 s (>= 1)
     t0 = time.perf_counter()
     coracle.sweep(u, wl.stencil, 1, f=f, omega=wl.omega, form="D", threads=threads)
@@ -233,16 +249,17 @@ def run_reference(args, wl, rank, world):
         times.append(time.perf_counter() - t0)
     ms = 1e3 * sum(times) / len(times)
     value = pts * sweeps / (ms / 1e3) / 1e9
-    sample = f"{sweeps} sweep(s) per step of the {note}, form D, C restatement, {threads} pthreads"
+    sample = (f"{sweeps} of {wl.sweeps} sweep(s) per step of the {note}, form D, C restatement, "
+              f"{threads} pthreads")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": workload_config(wl, world, {"parallelism": "host cores"}),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    del np
     print(json.dumps(line), flush=True)
 
 
@@ -452,9 +469,7 @@ def run_ours(args, wl, rank, world, local):
             "gpu_launches": int(launches),
             "clocks": clock_info,
             "e2e": e2e}
-    if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(wl)
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def main():
@@ -462,6 +477,9 @@ def main():
     rank, world, local = dist_env()
     wl = CONFIGS[args.config]
     if world > 1:
+        # NCCL init lines (rank/device/transport) for the multi-GPU record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
         if args.impl == "ours":
@@ -473,7 +491,16 @@ def main():
         if args.impl == "reference":
             run_reference(args, wl, rank, world)
         else:
-            run_ours(args, wl, rank, world, local)
+            line = run_ours(args, wl, rank, world, local)
+            if line is not None:
+                if world == 1 and not args.no_cpu_baseline:
+                    # after run_ours returned: its host/device buffers are freed first
+                    import gc
+                    import torch
+                    gc.collect()
+                    torch.cuda.empty_cache()
+                    line["cpu_baseline"] = cpu_baseline(wl)
+                print(json.dumps(line), flush=True)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -133,7 +133,9 @@ SL_API int sl_colour_pass(const sl_grid *g, const sl_stencil *s, int32_t colour,
                    int32_t *d_status, void *stream);
 
 /* In-place update of `count` mutually non-adjacent cells of grid 0 given as
- * device int64 flat indices — kernels.update_cells_batch (kernels.py:212-251). */
+ * device int64 flat indices — kernels.update_cells_batch (kernels.py:212-251).
+ * Like the reference, a batch with a non-finite result is not written at all:
+ * *d_status must be 0 on entry; it becomes non-zero and the grid is unchanged. */
 SL_API int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats,
                     int64_t count, int32_t *d_status, void *stream);
 

@@ -131,6 +131,30 @@ static int make_params(const sl_grid *g, const sl_stencil *s, int32_t *d_status,
 
 static bool empty_grid(const Params &p) { return p.nx == 0 || p.ny == 0 || p.nz == 0; }
 
+// Launches go to the device that owns the caller's stream (a tensor on a
+// non-current GPU comes with that GPU's stream): make it current for the call
+// and restore the caller's device afterwards.  The legacy/per-thread default
+// streams (0, 1, 2) belong to the current device.
+class StreamDevice {
+ public:
+  explicit StreamDevice(void *stream) {
+    if ((uintptr_t)stream <= 2 || cudaGetDevice(&prev_) != cudaSuccess) return;
+    int dev = prev_;
+    if (cudaStreamGetDevice((cudaStream_t)stream, &dev) == cudaSuccess && dev != prev_ &&
+        cudaSetDevice(dev) == cudaSuccess)
+      switched_ = true;
+  }
+  ~StreamDevice() {
+    if (switched_) cudaSetDevice(prev_);
+  }
+  StreamDevice(const StreamDevice &) = delete;
+  StreamDevice &operator=(const StreamDevice &) = delete;
+
+ private:
+  int prev_ = 0;
+  bool switched_ = false;
+};
+
 // Host version of plan.cuh's margin DP for any number of sweeps: the input
 // margin along axis `axis` that `sweeps` fused sweeps of `shape` consume.
 static int load_margin(int shape, int colours, int sweeps, int axis) {
@@ -193,6 +217,7 @@ size_t sl_workspace_bytes(const sl_grid *g, const sl_stencil *s) {
 
 int sl_colour_pass(const sl_grid *g, const sl_stencil *s, int32_t colour, int32_t *d_status,
                    void *stream) {
+  StreamDevice guard(stream);
   KernelKey key;
   Params p;
   int rc = make_params(g, s, d_status, &key, &p);
@@ -204,6 +229,7 @@ int sl_colour_pass(const sl_grid *g, const sl_stencil *s, int32_t colour, int32_
 
 int sl_sweep(const sl_grid *g, const sl_stencil *s, int32_t sweeps, uint32_t flags,
              double *workspace, size_t workspace_bytes, int32_t *d_status, void *stream) {
+  StreamDevice guard(stream);
   KernelKey key;
   Params p;
   int rc = make_params(g, s, d_status, &key, &p);
@@ -244,6 +270,7 @@ int sl_sweep(const sl_grid *g, const sl_stencil *s, int32_t sweeps, uint32_t fla
 static int sweep_pass_impl(const sl_grid *g, const sl_stencil *s, const double *src, double *dst,
                            int64_t zbegin, int64_t zend, double *pdn, int64_t dn_last, double *pup,
                            int64_t up_first, int32_t *d_status, void *stream) {
+  StreamDevice guard(stream);
   if (!g || !src || !dst || src == dst) return SL_E_INVAL;
   sl_grid gs = *g;
   gs.u = const_cast<double *>(src);
@@ -280,6 +307,7 @@ int sl_sweep_pass_peer(const sl_grid *g, const sl_stencil *s, const double *src,
 
 int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats, int64_t count,
                     int32_t *d_status, void *stream) {
+  StreamDevice guard(stream);
   KernelKey key;
   Params p;
   int rc = make_params(g, s, d_status, &key, &p);
@@ -290,6 +318,7 @@ int sl_update_cells(const sl_grid *g, const sl_stencil *s, const int64_t *d_flat
 
 int sl_sweep_cost(const sl_grid *g, const sl_stencil *s, const sl_cost *cost, int32_t sweeps,
                   uint32_t flags, int32_t *d_status, void *stream) {
+  StreamDevice guard(stream);
   KernelKey key;
   Params p;
   int rc = make_params(g, s, d_status, &key, &p);
@@ -318,6 +347,7 @@ int sl_sweep_cost(const sl_grid *g, const sl_stencil *s, const sl_cost *cost, in
 
 int sl_update_cells_cost(const sl_grid *g, const sl_stencil *s, const int64_t *d_flats,
                          int64_t count, const sl_cost *cost, int32_t *d_status, void *stream) {
+  StreamDevice guard(stream);
   KernelKey key;
   Params p;
   int rc = make_params(g, s, d_status, &key, &p);
@@ -339,6 +369,7 @@ int sl_ghost_depth(const sl_stencil *s, int32_t dim, int32_t sweeps) {
 }
 
 int sl_residual_max(const sl_grid *g, const sl_stencil *s, double *d_out, void *stream) {
+  StreamDevice guard(stream);
   KernelKey key;
   Params p;
   int rc = make_params(g, s, nullptr, &key, &p);

@@ -54,10 +54,16 @@ k1_colour_pass(Params p, int colour, RowMap rm) {
   }
 }
 
-template <int S, int FORM, bool UNIT, int DIV>
+// Indexed update in two stream-ordered launches, so that a batch with a
+// non-finite result leaves the mesh untouched like the reference
+// (kernels.py:243-251: the check precedes `u[F] = out`): COMMIT = false only
+// flags, COMMIT = true recomputes (the cells are mutually non-adjacent, so the
+// inputs are unchanged and the values identical) and stores iff no flag is set.
+template <int S, int FORM, bool UNIT, int DIV, bool COMMIT>
 __global__ void __launch_bounds__(256)
 k1_update_cells(Params p, const int64_t *__restrict__ flats, int64_t count) {
   constexpr int NNZ = shape_nnz(S);
+  if (COMMIT && *(volatile int32_t *)p.status != 0) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = flats[i];
@@ -66,8 +72,10 @@ k1_update_cells(Params p, const int64_t *__restrict__ flats, int64_t count) {
 #pragma unroll
     for (int j = 0; j < NNZ; ++j) acc = acc_add<FORM, UNIT>(acc, p.u[c + p.delta[j]], j, p);
     const double out = acc_finish<FORM, UNIT, DIV>(acc, uc, FORM == 1 ? p.f[c] : 0.0, p);
-    if (!finite64(out)) atomicOr(p.status, 1);
-    p.u[c] = out;
+    if (COMMIT)
+      p.u[c] = out;
+    else if (!finite64(out))
+      atomicOr(p.status, 1);
   }
 }
 
@@ -211,8 +219,9 @@ cudaError_t launch_update_cells(const KernelKey &key, const Params &p, const int
   int64_t blocks = (count + threads - 1) / threads;
   if (blocks > 148 * 64) blocks = 148 * 64;
   return dispatch(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
-    k1_update_cells<S, F, U, D><<<(unsigned)blocks, threads, 0, st>>>(p, flats, count);
-    note_launch();
+    k1_update_cells<S, F, U, D, false><<<(unsigned)blocks, threads, 0, st>>>(p, flats, count);
+    k1_update_cells<S, F, U, D, true><<<(unsigned)blocks, threads, 0, st>>>(p, flats, count);
+    note_launch(2);
     return cudaGetLastError();
   });
 }

@@ -389,11 +389,21 @@ static int64_t pick_chunks(int64_t cols, int64_t len, int64_t slots, int64_t ext
   return best;
 }
 
+// Resident-block count of a kernel variant on the current device, cached per
+// (thread, device): cudaFuncSetAttribute and the occupancy query are
+// per-device, so a second GPU used from the same thread gets its own entry.
+constexpr int MAX_DEVICES = 64;
+
 template <typename Kern>
-static cudaError_t prepare(Kern kern, size_t smem, int threads, int64_t *slots) {
+static cudaError_t prepare(Kern kern, size_t smem, int threads, int64_t (&cache)[MAX_DEVICES],
+                           int64_t *slots) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < MAX_DEVICES && cache[dev]) {
+    *slots = cache[dev];
+    return cudaSuccess;
+  }
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -404,6 +414,7 @@ static cudaError_t prepare(Kern kern, size_t smem, int threads, int64_t *slots) 
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
   *slots = (int64_t)(occ > 0 ? occ : 1) * sms;
+  if (dev >= 0 && dev < MAX_DEVICES) cache[dev] = *slots;
   return cudaSuccess;
 }
 
@@ -432,9 +443,10 @@ template <int S, int FORM, bool UNIT, int DIV, int M, bool PEER = false>
 static cudaError_t launch_stream3d(const Params &p, const double *src, double *dst, cudaStream_t st) {
     using G = Geo3<S, M>;
     auto kern = k2_stream3d<S, FORM, UNIT, DIV, M, PEER>;
-    static thread_local int64_t slots = 0;
-    if (!slots) {
-      cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
+    static thread_local int64_t cache[MAX_DEVICES] = {};  // resident blocks (per kernel variant)
+    int64_t slots = 0;
+    {
+      cudaError_t e = prepare(kern, G::SMEM, G::NT, cache, &slots);
       if (e != cudaSuccess) return e;
     }
     Tiles tl;
@@ -470,9 +482,10 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
   if constexpr (S == FD7 && M == 1) {
     using G = Col3Geo;
     auto kern = k2_col3d_fd7<FORM, UNIT, DIV, PEER>;
-    static thread_local int64_t slots = 0;
-    if (!slots) {
-      cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
+    static thread_local int64_t cache[MAX_DEVICES] = {};  // resident blocks (per kernel variant)
+    int64_t slots = 0;
+    {
+      cudaError_t e = prepare(kern, G::SMEM, G::NT, cache, &slots);
       if (e != cudaSuccess) return e;
     }
     CUtensorMap tmu, tmf;
@@ -489,9 +502,10 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     if (!q1_two_weights(p)) return launch_stream3d<S, FORM, UNIT, DIV, M, PEER>(p, src, dst, st);
     using G = Q1Geo;
     auto kern = k2_q1col<FORM, UNIT, DIV, PEER>;
-    static thread_local int64_t slots = 0;
-    if (!slots) {
-      cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
+    static thread_local int64_t cache[MAX_DEVICES] = {};  // resident blocks (per kernel variant)
+    int64_t slots = 0;
+    {
+      cudaError_t e = prepare(kern, G::SMEM, G::NT, cache, &slots);
       if (e != cudaSuccess) return e;
     }
     CUtensorMap tmu;
@@ -508,9 +522,10 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
   } else {
     using G = GeoS2<S, M>;
     auto run = [&](auto kern) -> cudaError_t {
-      static thread_local int64_t slots = 0;  // resident blocks (per kernel variant)
-      if (!slots) {
-        cudaError_t e = prepare(kern, G::SMEM, 32 * G::WPB, &slots);
+      static thread_local int64_t cache[MAX_DEVICES] = {};  // resident blocks (per kernel variant)
+      int64_t slots = 0;
+      {
+        cudaError_t e = prepare(kern, G::SMEM, 32 * G::WPB, cache, &slots);
         if (e != cudaSuccess) return e;
       }
       const int64_t Sx = p.nx + 2;
@@ -562,9 +577,10 @@ template <int S, int FORM, bool UNIT, int DIV, int M>
 static cudaError_t launch_block2d(const Params &p, const double *src, double *dst, cudaStream_t st) {
   using G = GeoB2<S, M>;
   auto kern = k4_block2d<S, FORM, UNIT, DIV, M>;
-  static thread_local int64_t slots = 0;
-  if (!slots) {
-    cudaError_t e = prepare(kern, G::SMEM, G::NT, &slots);
+  static thread_local int64_t cache[MAX_DEVICES] = {};  // resident blocks (per kernel variant)
+  int64_t slots = 0;
+  {
+    cudaError_t e = prepare(kern, G::SMEM, G::NT, cache, &slots);
     if (e != cudaSuccess) return e;
   }
   const int64_t Sx = p.nx + 2, Sy = p.ny + 2;

@@ -54,6 +54,9 @@ struct GeoS2 {
   static constexpr int SLOTB = 2 * ROWB;               // u + f
   static constexpr size_t SMEM = size_t(WPB) * NS * SLOTB;
   static_assert(NRR >= NRR0, "register ring too short");
+  // ring indices (KS % NS, (KS + 1) % NRR over an unroll of U) wrap correctly only
+  // for power-of-two depths that divide U
+  static_assert((NS & (NS - 1)) == 0 && U % NS == 0 && U % NRR == 0, "STRIP_NS must be a power of two");
   // does the stencil use offset (dx, dy)?
   static constexpr bool uses(int dx, int dy) {
     for (int q = 0; q < shape_nnz(S); ++q) {

@@ -98,18 +98,24 @@ k5_cost_phase(Params p, CostSpec cs, int colour, int64_t h, int64_t xw, int64_t 
   flush_work(work, cs.work);
 }
 
-template <int S, int FORM>
+// Two launches like k1_update_cells: COMMIT = false flags and tallies the
+// sine work, COMMIT = true stores iff nothing was flagged (values are
+// bitwise independent of k, so the commit pass runs with k = 0).
+template <int S, int FORM, bool COMMIT>
 __global__ void __launch_bounds__(128)
 k5_cost_cells(Params p, CostSpec cs, const int64_t *__restrict__ flats, int64_t count) {
+  if (COMMIT && *(volatile int32_t *)p.status != 0) return;
   double work = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = flats[i];
-    const double out = cost_update<S, FORM>(p, p.u, p.f, c, cs.k, work);
-    if (!finite64(out)) atomicOr(p.status, 1);
-    p.u[c] = out;
+    const double out = cost_update<S, FORM>(p, p.u, p.f, c, COMMIT ? 0 : cs.k, work);
+    if (COMMIT)
+      p.u[c] = out;
+    else if (!finite64(out))
+      atomicOr(p.status, 1);
   }
-  flush_work(work, cs.work);
+  if (!COMMIT) flush_work(work, cs.work);
 }
 
 KernelKey generic(KernelKey k) {
@@ -172,8 +178,9 @@ cudaError_t launch_cost_cells(const KernelKey &key, const Params &p, const CostS
     if constexpr (U || D) {
       return cudaErrorNotSupported;
     } else {
-      k5_cost_cells<S, F><<<blocks_for(count, threads), threads, 0, st>>>(p, c, flats, count);
-      note_launch();
+      k5_cost_cells<S, F, false><<<blocks_for(count, threads), threads, 0, st>>>(p, c, flats, count);
+      k5_cost_cells<S, F, true><<<blocks_for(count, threads), threads, 0, st>>>(p, c, flats, count);
+      note_launch(2);
       return cudaGetLastError();
     }
   });

@@ -200,7 +200,7 @@ class CostModel:
 class DeviceCall:
     """C-ABI descriptors + status word for one (mesh, kind) pair."""
 
-    __slots__ = ("mesh", "kind", "grid", "stencil", "status", "stream", "_torch")
+    __slots__ = ("mesh", "kind", "grid", "stencil", "status", "stream", "_torch", "_u", "_f")
 
     def __init__(self, mesh: Mesh, kind: StencilKind):
         if kind.dim != mesh.dim:
@@ -218,11 +218,14 @@ class DeviceCall:
         g.batch = 1
         g.batch_stride = mesh.size
         g.u = u.data_ptr()
+        self._u = u                 # the descriptor's pointers stay owned while bound
+        self._f = None
         form = _native.SL_FORM_R
         omega = 0.0
         if mesh.has_rhs:
             form = _native.SL_FORM_D
-            g.f = mesh.rhs_device().data_ptr()
+            self._f = mesh.rhs_device()
+            g.f = self._f.data_ptr()
             omega = mesh.omega
         self.grid = g
         self.stencil = kind.descriptor(form, omega)
@@ -230,8 +233,15 @@ class DeviceCall:
         self.stream = torch.cuda.current_stream(u.device).cuda_stream
 
     def refresh(self):
-        """Re-bind after host edits (the device tensor is reused in place)."""
-        self.grid.u = self.mesh.device_values().data_ptr()
+        """Re-bind u and f before a call: host edits of `values` are uploaded,
+        and a right-hand side replaced since the last call (`set_rhs`,
+        `init_rhs`) is re-read — the descriptor never keeps a freed f."""
+        self._u = self.mesh.device_values()
+        self.grid.u = self._u.data_ptr()
+        if self.mesh.has_rhs:
+            self._f = self.mesh.rhs_device()
+            self.grid.f = self._f.data_ptr()
+        self.stream = self._torch.cuda.current_stream(self._u.device).cuda_stream
 
     def check_status(self, what: str):
         flag = int(self.status.item())

@@ -140,6 +140,7 @@ class SlabRunner:
         self.f = None
         self.omega = None
         self._pass = compute or self._gpu_pass   # (src, dst, z0, z1): one sweep into dst planes [z0, z1)
+        self._residual = None                    # tests: (runner) -> local max over the owned planes
         self._desc = None
         self._fused = None
         self._status = None
@@ -400,6 +401,46 @@ class SlabRunner:
             count -= k
         if self._pass == self._gpu_pass:
             self.check_status()
+
+    # -- residual (reference kernels.py:254-265, convergence loop bench.py:445-474) --
+
+    def _gpu_residual(self) -> float:
+        """max |f - A u| (|A u| without f) over this rank's owned planes, on the
+        device: sl_residual_max over a window whose interior is the owned
+        planes and whose halo planes are the ghost planes around them."""
+        import torch
+        lib = _native.require_cuda()
+        g0, st = self._descriptors()
+        L = self.layout
+        off = (L.a - L.lo - 1) * self.plane_elems() * 8
+        g = _native.SlGrid()
+        ctypes.memmove(ctypes.byref(g), ctypes.byref(g0), ctypes.sizeof(g))
+        g.n[self.dim - 1] = L.b - L.a + 1
+        g.origin[self.dim - 1] = 0
+        g.u = self.u.data_ptr() + off
+        if self.f is not None:
+            g.f = self.f.data_ptr() + off
+        out = torch.zeros(1, dtype=torch.float64, device=self.device)
+        rc = lib.sl_residual_max(ctypes.byref(g), ctypes.byref(st), out.data_ptr(),
+                                 torch.cuda.current_stream(self.device).cuda_stream)
+        _native.check(rc, "slab residual")
+        return float(out.item())
+
+    def residual_max(self) -> float:
+        """Residual of the global grid's current state: each rank reduces its
+        owned planes (the exchanged ghost planes supply their neighbours),
+        then all_reduce(MAX) — equal to the single-domain residual_max bit for
+        bit (a max does not depend on the order it is taken in)."""
+        import torch
+        local = self._residual(self) if self._residual is not None else self._gpu_residual()
+        if self.world == 1:
+            return local
+        import torch.distributed as dist
+        on_gpu = dist.get_backend(self.group) == "nccl"
+        t = torch.tensor([local], dtype=torch.float64,
+                         device=self.device if on_gpu else torch.device("cpu"))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
 
     def owned(self):
         """This rank's owned planes (global [a, b]) as a view."""

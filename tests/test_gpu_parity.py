@@ -149,10 +149,10 @@ def test_config3_fd7_514_full():
     assert _bits_equal(got, want)
 
 
-def test_config4_fe27q1_1026_two_sweeps():
-    # full 1026^3 grid; 2 of the 10 sweeps keep the CPU oracle to ~a minute
-    want = _oracle_d("fe27q1", 1024, 2)
-    got = _gpu_d("fe27q1", 1024, 2)
+def test_config4_fe27q1_1026_full():
+    # the full BASELINE config: 1026^3 grid, all 10 sweeps (C oracle on all host threads)
+    want = _oracle_d("fe27q1", 1024, 10)
+    got = _gpu_d("fe27q1", 1024, 10)
     assert _bits_equal(got, want)
 
 
@@ -188,8 +188,33 @@ def test_nonfinite_raises_numerics_error():
         sl.run_sweeps(m, sl.FD5, sl.CostModel(), 2)
     m = sl.make_mesh(2, 4, seed=1)
     m.values[m.flat_index((0, 1))] = np.nan
+    before = m.values.copy()
+    flats = np.array([m.flat_index((1, 1)), m.flat_index((3, 3)), m.flat_index((2, 4))])
     with pytest.raises(sl.NumericsError):
-        sl.update_cells_batch(m, sl.FD5, np.array([m.flat_index((1, 1))]), 0)
+        sl.update_cells_batch(m, sl.FD5, flats, 0)
+    # like the reference (kernels.py:243-251) the failing batch writes nothing
+    assert _bits_equal(m.values, before)
+    with pytest.raises(sl.NumericsError):
+        sl.update_cells_batch(m, sl.FD5, flats, 3)
+    assert _bits_equal(m.values, before)
+
+
+def test_replaced_rhs_is_used_by_a_reused_plan():
+    """set_rhs with the same omega after a sweep: the cached plan must read
+    the new f (it once kept the freed tensor's pointer)."""
+    for name, n in (("fe9", 40), ("fe27q1", 12)):
+        kind = sl.get_stencil(name)
+        m = sl.make_mesh(kind.dim, n, seed=5)
+        sl.init_rhs(m, 6, 0.8)
+        plan = sl.SweepPlan(m, kind, sl.CostModel())
+        sl.run_sweeps(m, kind, sl.CostModel(), 2, plan=plan)
+        f2 = R.init_f(kind.dim, n, 99)
+        m.set_rhs(f2.reshape(-1).copy(), 0.8)
+        sl.run_sweeps(m, kind, sl.CostModel(), 3, plan=plan)
+        u = R.init_u(kind.dim, n, 5)
+        coracle.sweep(u, name, 2, f=R.init_f(kind.dim, n, 6), omega=0.8, form="D")
+        coracle.sweep(u, name, 3, f=f2, omega=0.8, form="D")
+        assert _bits_equal(m.values, u), name
 
 
 def test_constant_mesh_unchanged():

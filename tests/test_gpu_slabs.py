@@ -17,7 +17,7 @@ from paper_1810_04033_b200.slabs import SlabRunner
 pytestmark = pytest.mark.gpu
 
 
-def _emulated(name, n, sweeps, world, per, overlap=False):
+def _emulated(name, n, sweeps, world, per, overlap=False, runners=None):
     kind = sl.get_stencil(name)
     rs = [SlabRunner(kind.dim, n, kind, world=world, rank=r, ghost_sweeps=per, device="cuda",
                      overlap=overlap) for r in range(world)]
@@ -35,6 +35,8 @@ def _emulated(name, n, sweeps, world, per, overlap=False):
             r0.u[L0.b + 1 - L0.lo:].copy_(r1.u[L0.b + 1 - L1.lo:L0.hi + 1 - L1.lo])
     for r in rs:
         r.check_status()
+    if runners is not None:
+        runners.extend(rs)
     out = np.zeros((n + 2,) * kind.dim)
     for i, r in enumerate(rs):
         L = r.layout
@@ -106,3 +108,20 @@ def test_emulated_peer_exchange_equals_single_domain(name, n, sweeps, world, per
             assert np.array_equal(r.u[0:L.a - L.lo].cpu().numpy(),
                                   rs[i - 1].u[L.lo - Lp.lo:L.a - Lp.lo].cpu().numpy())
     assert np.array_equal(out.view(np.int64), want.view(np.int64))
+
+
+@pytest.mark.parametrize("name,n,world", [("fd7", 40, 3), ("fe27q1", 30, 2), ("fe9", 130, 4)])
+def test_emulated_slab_residual_equals_single_domain(name, n, world):
+    """Each slab's device residual over its owned planes; the max over the
+    slabs (what all_reduce(MAX) returns) equals the whole-grid residual."""
+    dim = R.STENCIL_TABLE[name][0]
+    rs = []
+    _emulated(name, n, 3, world, 1, runners=rs)
+    want = R.init_u(dim, n, 7)
+    f = R.init_f(dim, n, 8)
+    coracle.sweep(want, name, 3, f=f, omega=0.8, form="D")
+    assert max(r._gpu_residual() for r in rs) == R.residual_max(want, name, f)
+    one = SlabRunner(dim, n, sl.get_stencil(name), device="cuda")
+    one.init(7, 8, 0.8)
+    one.sweep(3)
+    assert one.residual_max() == R.residual_max(want, name, f)

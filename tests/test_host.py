@@ -166,3 +166,21 @@ def test_device_entry_points_fail_loudly_without_cuda():
     m = sl.make_mesh(2, 4, seed=1)
     with pytest.raises(NativeLibraryError):
         sl.run_sweep("colouring", m, sl.FD5, sl.CostModel(), pool=sl.DevicePool())
+
+
+def test_stencil_lab_import_name_reaches_the_gpu_package():
+    """`import stencil_lab` is the reference's import name (reference
+    __init__.py:8-27); its modules are this package's."""
+    import stencil_lab
+    import stencil_lab.bench
+    import stencil_lab.kernels
+    import stencil_lab.mesh
+    import stencil_lab.strategies
+    from stencil_lab.taskrt import Schedule
+    assert stencil_lab.strategies is strategies
+    assert stencil_lab.bench.StrategyRunner is runner.StrategyRunner
+    assert stencil_lab.sweep_colouring is sl.sweep_colouring
+    assert stencil_lab.make_mesh is sl.make_mesh
+    assert Schedule is sl.Schedule
+    with pytest.raises(ImportError, match="nested dissection"):
+        from stencil_lab import dissect  # noqa: F401

@@ -39,6 +39,25 @@ def oracle_pass(runner, name):
     return run
 
 
+def oracle_residual(name):
+    """max |f - A u| over a runner's owned planes (CPU stand-in for sl_residual_max)."""
+    def run(runner):
+        dim, offsets, weights, wc, _ = R.STENCIL_TABLE[name]
+        L = runner.layout
+        u, f = runner.u.numpy(), runner.f.numpy()
+        a, b, n = L.a - L.lo, L.b - L.lo, runner.n
+        inner = (slice(a, b + 1),) + (slice(1, n + 1),) * (dim - 1)
+        acc = wc * u[inner]
+        for off, w in zip(offsets, weights):
+            if w == 0.0:
+                continue
+            o = tuple(reversed(off))     # (slow axis, ..., x)
+            nb = (slice(a + o[0], b + 1 + o[0]),) + tuple(slice(1 + d, n + 1 + d) for d in o[1:])
+            acc += w * u[nb]
+        return float(np.abs(f[inner] - acc).max())
+    return run
+
+
 def _worker(rank, world, port, case, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -58,11 +77,13 @@ def _run(rank, world, case, q):
         r = SlabRunner(kind.dim, n, kind, world=world, rank=rank, ghost_sweeps=per,
                        ghost=2 * per, overlap=n >= 20)   # n >= 20: boundary / interior split
         r._pass = oracle_pass(r, name)
+        r._residual = oracle_residual(name)
         r.init(7, 8, 0.8)
         r.sweep(sweeps)
+        res = r.residual_max()          # all_reduce(MAX) over the ranks' owned planes
         out = r.gather()
         if rank == 0:
-            q.put(out)
+            q.put((out, res))
 
 
 CASES = [("fd7", 11, 5, 2), ("fe9", 14, 4, 1), ("fe27q1", 10, 3, 1), ("fd5", 16, 6, 3), ("fd7", 20, 4, 4),
@@ -85,10 +106,12 @@ def test_two_rank_slabs_equal_single_domain(case):
     got = q.get(timeout=120)
     if isinstance(got, Exception):
         raise got
+    got, res = got
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert np.array_equal(got.view(np.int64), want.view(np.int64))
+    assert res == R.residual_max(want, name, f)
 
 
 def test_layout_covers_grid():
