@@ -31,7 +31,9 @@
 
 #include <cudaTypedefs.h>
 
+#include <mutex>
 #include <utility>
+#include <vector>
 
 namespace sl {
 
@@ -419,8 +421,42 @@ static cudaError_t prepare(Kern kern, size_t smem, int threads, int64_t (&cache)
 }
 
 // 3D fp64 tensor map over a dense (n+2)^3 grid with a 64 x 32 x 1 box.
+// Encoded maps are cached per (base, extents, strides, box): a sweep's passes
+// alternate between two buffers, so after the first two passes no pass
+// re-encodes (the cache is small and cleared when full).
+struct TmapKey {
+  const double *base;
+  int64_t nx, ny, nz, sy, sz;
+  int boxx, boxy;
+  bool operator==(const TmapKey &o) const {
+    return base == o.base && nx == o.nx && ny == o.ny && nz == o.nz && sy == o.sy && sz == o.sz &&
+           boxx == o.boxx && boxy == o.boxy;
+  }
+};
+
+static cudaError_t encode_tmap3(CUtensorMap *map, const double *base, const Params &p, int boxx,
+                                int boxy);
+
 static cudaError_t make_tmap3(CUtensorMap *map, const double *base, const Params &p,
                               int boxx = Col3Geo::PX, int boxy = Col3Geo::PY) {
+  static std::mutex mu;
+  static std::vector<std::pair<TmapKey, CUtensorMap>> cache;
+  const TmapKey key{base, p.nx, p.ny, p.nz, p.sy, p.sz, boxx, boxy};
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto &e : cache)
+    if (e.first == key) {
+      *map = e.second;
+      return cudaSuccess;
+    }
+  const cudaError_t e = encode_tmap3(map, base, p, boxx, boxy);
+  if (e != cudaSuccess) return e;
+  if (cache.size() >= 32) cache.clear();
+  cache.emplace_back(key, *map);
+  return cudaSuccess;
+}
+
+static cudaError_t encode_tmap3(CUtensorMap *map, const double *base, const Params &p, int boxx,
+                                int boxy) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;

@@ -61,7 +61,7 @@ class SweepPipeline:
             g.batch_stride = side * side if batch else u.numel()
             g.u = u.data_ptr()
             g.f = f.data_ptr() if f is not None else None
-            nb = 0 if flags else self._lib.sl_workspace_bytes(ctypes.byref(g), ctypes.byref(self._stencil))
+            nb = 0 if flags & ~_native.SL_FLAG_STREAM else self._lib.sl_workspace_bytes(ctypes.byref(g), ctypes.byref(self._stencil))
             ws = torch.empty((nb + 7) // 8, dtype=torch.float64, device=self.device) if nb else None
             self._slots.append({
                 "u": u, "f": f, "grid": g, "ws": ws, "ws_bytes": nb,

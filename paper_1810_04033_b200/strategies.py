@@ -143,7 +143,8 @@ def run_sweeps(mesh: Mesh, kind: StencilKind, cost: CostModel, sweeps: int,
         return float(work.item())
     ws_bytes = 0
     ws_ptr = None
-    if not flags:
+    if not flags & (_native.SL_FLAG_PER_COLOUR | _native.SL_FLAG_MERGE_COLOURS | _native.SL_FLAG_LEX):
+        # the fused kernels (SL_FLAG_STREAM included) ping-pong through a workspace
         ws_bytes = lib.sl_workspace_bytes(ctypes.byref(call.grid), ctypes.byref(call.stencil))
         ws = mesh.workspace(ws_bytes)
         ws_ptr = ws.data_ptr() if ws is not None else None
