@@ -73,10 +73,14 @@ constexpr bool q1_plan_ok() {
 }
 static_assert(q1_plan_ok(), "unexpected plan");
 
-template <int FORM, bool UNIT, int DIV, bool PEER = false>
-__global__ void __launch_bounds__(Q1Geo::NT, 1)
-k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__ dst, int64_t ntx,
-         int64_t nty, int64_t nzc) {
+// EDGE = false: the tile's whole window lies inside the grid interior in x
+// and y, so no point needs a mask — every computed point may be updated (points
+// outside their phase's need region hold values nobody needed reads, plan.cuh)
+// and only owned points are checked for non-finite results, when stored.
+// EDGE = true keeps the per-point interior/need masks.
+template <int FORM, bool UNIT, int DIV, bool PEER, bool EDGE>
+__device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &tmu, double *__restrict__ dst,
+                                           int64_t ntx, int64_t nty, int64_t nzc) {
   using G = Q1Geo;
   constexpr FPlan P = G::P;
   constexpr int RT = G::RT, H = RT / 2, RR = G::RR;
@@ -163,10 +167,14 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   const int64_t rowoff0 = (int64_t)(gy0 + r0) * p.sy + gx;   // row r0 of this thread
   const int sy32 = (int)p.sy;
 #pragma unroll
+  unsigned inbits = 0;   // interior (updated) points: bit 2*a + s
   for (int a = 0; a < RT; ++a) {
     const int r = r0 + a, gy = gy0 + r;
     ownbits |= (colown && r >= G::GY && r < G::GY + TYo) ? (1u << a) : 0u;
     fokbits |= (gy >= 0 && gy < Sy && gx >= 0 && gx + 1 < Sx) ? (1u << a) : 0u;
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+      inbits |= (gy >= 1 && gy <= ny && gx + s >= 1 && gx + s <= nx) ? (1u << (2 * a + s)) : 0u;
   }
 
   // own rows of planes pp-2 .. pp+1: [row][ring][col]; plane P at (P - base) % RR
@@ -236,7 +244,13 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
     constexpr int RC = (RP - LAGG + RR) % RR;      // ring entry of plane pz
     constexpr int NZJ = cmax(P.need[2 * GI][2], P.need[2 * GI + 1][2]);
     const int pz = pp - LAGG;
-    const bool okz = pz >= 1 && pz <= nz && pz >= z0 - NZJ && pz < z1 + NZJ;
+    // CTA-uniform.  Planes beyond the chunk's need range are computed like
+    // ghost points (nobody needed reads them); boundary planes and planes
+    // outside the grid are computed too but their results are dropped after
+    // the group (a branch around the whole group would wrap every shuffle in
+    // convergence code)
+    const bool pzin = pz >= 1 && pz <= nz;
+    (void)NZJ;
     double acc[H][2];
 #pragma unroll
     for (int h = 0; h < H; ++h)
@@ -312,7 +326,7 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
     for (int h = 0; h < H; ++h)
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
-        ok[h][s] = okz && ((okbits >> (4 * GI + 2 * h + s)) & 1u);
+        ok[h][s] = !EDGE || ((okbits >> (4 * GI + 2 * h + s)) & 1u);
         a[h][s] = FORM == 0 ? acc[h][s] : __dsub_rn(s == 0 ? fv[h].x : fv[h].y, acc[h][s]);
         if (DIV == DIV_RCP) {
           const double e = __dmul_rn(a[h][s], p.rwc);
@@ -334,7 +348,8 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
           if (ok[h][s] && (xe - (64u << 20)) >= (1919u << 20)) q[h][s] = q1_div_exact(a[h][s], p.wc);
         }
     }
-    // commit: ring, non-finite tally, publish to the plane's slot
+    // commit: ring, publish to the plane's slot (a dropped plane gets its
+    // unchanged values back from the slot)
     double *pc = slot_of(pz);
 #pragma unroll
     for (int h = 0; h < H; ++h) {
@@ -342,26 +357,44 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
       for (int s = 0; s < 2; ++s) {
         const double uc = U[A + 2 * h][RC][s];
         const double out = FORM == 0 ? q[h][s] : __dadd_rn(uc, __dmul_rn(p.omega, q[h][s]));
-        const unsigned ex = (unsigned)__double2hiint(out) & 0x7ff00000u;
-        emax = max(emax, ok[h][s] ? ex : 0u);
-        U[A + 2 * h][RC][s] = ok[h][s] ? out : uc;
+        U[A + 2 * h][RC][s] = (!EDGE || ok[h][s]) ? out : uc;
       }
-      *reinterpret_cast<double2 *>(pc + (A + 2 * h) * G::PX) =
-          make_double2(U[A + 2 * h][RC][0], U[A + 2 * h][RC][1]);
+    }
+    if (pzin) {
+#pragma unroll
+      for (int h = 0; h < H; ++h)
+        *reinterpret_cast<double2 *>(pc + (A + 2 * h) * G::PX) =
+            make_double2(U[A + 2 * h][RC][0], U[A + 2 * h][RC][1]);
+    } else {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const double2 v = *reinterpret_cast<const double2 *>(pc + (A + 2 * h) * G::PX);
+        U[A + 2 * h][RC][0] = v.x;
+        U[A + 2 * h][RC][1] = v.y;
+      }
     }
   };
 
-  // owned rows of a final plane (ring entry RE) -> dst
+  // owned rows of a final plane (ring entry RE) -> dst; the non-finite check
+  // covers exactly the updated points of the pass: owned and interior
   double *const dthr = dst + rowoff0;
   auto store_plane = [&](int po, auto RE) {
     constexpr int E = decltype(RE)::value;
     if (po >= z0 && po < z1) {
       double *dp = dthr + (int64_t)po * sz;
+      const bool zin = po >= 1 && po <= nz;
 #pragma unroll
       for (int a = 0; a < RT; ++a)
         if ((ownbits >> a) & 1u) {
           stg_pair(dp + a * sy32, U[a][E][0], U[a][E][1]);
           stg_pair_peers<PEER>(p, po, (int64_t)po * sz + rowoff0 + a * sy32, U[a][E][0], U[a][E][1]);
+          if (zin) {
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const unsigned ex = (unsigned)__double2hiint(U[a][E][s]) & 0x7ff00000u;
+              emax = max(emax, (!EDGE || ((inbits >> (2 * a + s)) & 1u)) ? ex : 0u);
+            }
+          }
         }
     }
   };
@@ -418,6 +451,26 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   __syncthreads();
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (__any_sync(0xffffffffu, emax == 0x7ff00000u) && lane == 0) atomicOr(p.status, 1);
+}
+
+template <int FORM, bool UNIT, int DIV, bool PEER = false>
+__global__ void __launch_bounds__(Q1Geo::NT, 1)
+k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__ dst, int64_t ntx,
+         int64_t nty, int64_t nzc) {
+  using G = Q1Geo;
+  // interior tile: its loaded window [x0 - GX, x0 - GX + PX) x [y0 - GY, y0 - GY + BOXY)
+  // lies in [1, n] in x and y (same tile arithmetic as the body)
+  const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2;
+  const int item = blockIdx.x;
+  const int tx = item % (int)ntx, ty = (item / (int)ntx) % (int)nty;
+  const int x0 = (int)(2 * (((int64_t)tx * (Sx / 2)) / ntx));
+  const int y0 = (int)(((int64_t)ty * Sy) / nty);
+  const bool edge = x0 - G::GX < 1 || x0 - G::GX + G::PX > (int)p.nx + 1 || y0 - G::GY < 1 ||
+                    y0 - G::GY + G::BOXY > (int)p.ny + 1;
+  if (edge)
+    q1col_body<FORM, UNIT, DIV, PEER, true>(p, tmu, dst, ntx, nty, nzc);
+  else
+    q1col_body<FORM, UNIT, DIV, PEER, false>(p, tmu, dst, ntx, nty, nzc);
 }
 
 }  // namespace sl
