@@ -29,7 +29,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1810_04033_b200.configs import BYTES_PER_UPDATE, CONFIGS  # noqa: E402
+from paper_1810_04033_b200.configs import BYTES_PER_UPDATE, CONFIGS, FP64_OPS_PER_UPDATE  # noqa: E402
 
 METRIC = "fp64 grid-point updates/s (GLUP/s)"
 UNIT = "GLUP/s"
@@ -67,6 +67,15 @@ def peaks():
         return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def fp64_peak():
+    """Measured fp64 instruction peak of the box (tools/fp64_peak.cu, DADD rate)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")) as fh:
+            return float(json.load(fh)["dadd_ops_per_s"]) / 1e12, "measured (profiles/r02_fp64_peak.json, DADD)"
+    except Exception:
+        return 148 * 64 * 1.965e9 / 1e12, "nominal 64 fp64 lanes/SM/clk x 148 SMs x 1.965 GHz"
 
 
 def ncu_traffic(workload_name):
@@ -469,6 +478,19 @@ def run_ours(args, wl, rank, world, local):
             "gpu_launches": int(launches),
             "clocks": clock_info,
             "e2e": e2e}
+    if wl.batch > 1 and not args.per_colour:
+        # config 5 keeps every patch on chip for all sweeps: the fp64 pipe bounds it, not HBM
+        # (K3 Form D FD5: DMUL w_c u, 4 DSUB, DSUB f - Au, DMUL 1/w_c, DMUL omega, DADD = 9
+        # fp64 instructions = 9 flops per update, no FMA)
+        fpk, fsrc = fp64_peak()
+        fach = FP64_OPS_PER_UPDATE[wl.index] * total_updates / world / (ms_per_step / 1e3) / 1e12
+        hbm = line["roofline"]
+        line["roofline"] = {"bound": "fp64", "achieved": fach, "peak": fpk, "unit": "TFLOP/s",
+                            "frac": fach / fpk, "traffic": hbm["traffic"], "peak_source": fsrc,
+                            "algorithmic_ops": f"{FP64_OPS_PER_UPDATE[wl.index]} fp64 instructions per update",
+                            "hbm_24B_accounting": {"achieved": hbm["achieved"], "peak": hbm["peak"],
+                                                   "unit": "GB/s", "frac": hbm["frac"]},
+                            "launches_per_step": hbm["launches_per_step"]}
     return line
 
 

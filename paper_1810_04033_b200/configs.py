@@ -10,10 +10,14 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-__all__ = ["Workload", "CONFIGS", "BYTES_PER_UPDATE"]
+__all__ = ["Workload", "CONFIGS", "BYTES_PER_UPDATE", "FP64_OPS_PER_UPDATE"]
 
 # algorithmic bytes per grid-point update: read u_c + read f_c + write u_c
 BYTES_PER_UPDATE = 24
+
+# fp64 instructions per update of the on-chip (fp64-bound) patch kernel, config 5
+# (K3, Form D FD5: DMUL w_c*u, 4 DSUB, DSUB f-Au, DMUL 1/w_c, DMUL omega, DADD)
+FP64_OPS_PER_UPDATE = {5: 9}
 
 
 @dataclass(frozen=True)

@@ -707,13 +707,22 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
   }
   // FD5 (red-black 2D) fuses two sweeps per pass: half the passes, and the
   // 2-sweep ghost (4 columns/rows) still fits a 64-column strip
+#ifdef SL_FE9_M2
+  const bool two = (key.shape == FD5 || key.shape == FE9) && sweeps >= 2;
+#else
   const bool two = key.shape == FD5 && sweeps >= 2;
+#endif
   for (int s = 0; s < sweeps && e == cudaSuccess;) {
     const int m = (two && sweeps - s >= 2) ? 2 : 1;
     e = dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
       if constexpr (S == FD5)
         return m == 2 ? launch_pass<S, F, U, D, 2>(p, bufs[cur], bufs[cur ^ 1], st)
                       : launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
+#ifdef SL_FE9_M2
+      else if constexpr (S == FE9)
+        return m == 2 ? launch_pass<S, F, U, D, 2>(p, bufs[cur], bufs[cur ^ 1], st)
+                      : launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
+#endif
       else
         return launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
     });
