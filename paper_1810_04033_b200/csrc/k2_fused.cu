@@ -707,7 +707,15 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
   }
   // FD5 (red-black 2D) fuses two sweeps per pass: half the passes, and the
   // 2-sweep ghost (4 columns/rows) still fits a 64-column strip
-#ifdef SL_FE9_M2
+  // FD5 and FE9 fuse two sweeps per pass (FE9: 241 vs 230 GLUP/s on config 2,
+  // DESIGN.md §8); -DSL_NO_FE9_M2 restores one FE9 sweep per pass, -DSL_FD7_M2 runs
+  // FD7 two sweeps per pass through the generic stream kernel (A/B only)
+#ifndef SL_NO_FE9_M2
+#define SL_FE9_M2
+#endif
+#ifdef SL_FD7_M2
+  const bool two = (key.shape == FD5 || key.shape == FE9 || key.shape == FD7) && sweeps >= 2;
+#elif defined(SL_FE9_M2)
   const bool two = (key.shape == FD5 || key.shape == FE9) && sweeps >= 2;
 #else
   const bool two = key.shape == FD5 && sweeps >= 2;
@@ -721,6 +729,11 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
 #ifdef SL_FE9_M2
       else if constexpr (S == FE9)
         return m == 2 ? launch_pass<S, F, U, D, 2>(p, bufs[cur], bufs[cur ^ 1], st)
+                      : launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
+#endif
+#ifdef SL_FD7_M2
+      else if constexpr (S == FD7)
+        return m == 2 ? launch_stream3d<S, F, U, D, 2>(p, bufs[cur], bufs[cur ^ 1], st)
                       : launch_pass<S, F, U, D, 1>(p, bufs[cur], bufs[cur ^ 1], st);
 #endif
       else
