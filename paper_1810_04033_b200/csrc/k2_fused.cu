@@ -28,6 +28,7 @@
 #include "k3_patch.cuh"
 #include "k2_col3d.cuh"
 #include "k2_q1col.cuh"
+#include "k6_resident2d.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -365,10 +366,19 @@ static bool fused_supported(const KernelKey &key, const Params &p) {
   return true;
 }
 
+// K6 (resident red-black 2D) needs two exchange grids and the tile flags
+constexpr size_t K6_FLAG_BYTES = 4096;
+
+static bool resident_candidate(const KernelKey &key, const Params &p) {
+  return key.shape == FD5 && key.unit && key.div == DIV_POW2 && p.colours == 2 && p.px == 0 &&
+         p.py == 0 && (p.nx + 2) * (p.ny + 2) <= (int64_t)4 * 1024 * 1024;
+}
+
 #ifndef SL_PEER_TU
 size_t fused_workspace_bytes(const KernelKey &key, const Params &p) {
   if (!fused_supported(key, p)) return 0;
   const int64_t elems = (p.nx + 2) * (p.ny + 2) * (shape_dim(key.shape) == 3 ? (p.nz + 2) : 1);
+  if (resident_candidate(key, p)) return (size_t)(2 * elems) * sizeof(double) + K6_FLAG_BYTES;
   return (size_t)elems * sizeof(double);
 }
 #endif
@@ -603,6 +613,56 @@ static cudaError_t launch_patches(const KernelKey &key, const Params &p, int swe
   return e;
 }
 
+// K6: the whole red-black 2D grid resident on chip (one tile per SM, cooperative
+// launch), rounds of M sweeps between exchanges; the largest M whose tiling fits
+// the co-resident CTAs (fewest exchanges: a tile's compute per sweep does not
+// depend on M).  Returns cudaErrorNotSupported when no tiling fits.
+template <int FORM, bool UNIT, int DIV, int M>
+static cudaError_t launch_resident_m(const Params &p, double *ws, int sweeps, cudaStream_t st) {
+  using R = ResGeo;
+  auto kern = k6_resident2d<FORM, UNIT, DIV, M>;
+  static thread_local int64_t cache[MAX_DEVICES] = {};
+  int64_t slots = 0;
+  {
+    cudaError_t e = prepare(kern, R::SMEM, R::NT, cache, &slots);
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t Sx = p.nx + 2, Sy = p.ny + 2;
+  int ntx = (int)((Sx + R::own_w(M) - 1) / R::own_w(M));
+  while (2 * ((Sx / 2 + ntx - 1) / ntx) > R::own_w(M)) ++ntx;   // even tile starts
+  const int nty = (int)((Sy + R::own_h(M) - 1) / R::own_h(M));
+  if ((int64_t)ntx * nty > slots || (int64_t)ntx * nty * 4 > (int64_t)K6_FLAG_BYTES) return cudaErrorNotSupported;
+  // every tile must own at least its ghost width, so only the 8 neighbours read it
+  if (Sx / ntx < 2 * M + 2 || Sy / nty < 2 * M + 2) return cudaErrorNotSupported;
+  const int64_t elems = Sx * Sy;
+  double *ex0 = ws, *ex1 = ws + elems;
+  int *flags = reinterpret_cast<int *>(ws + 2 * elems);
+  cudaError_t e = cudaMemsetAsync(flags, 0, (size_t)ntx * nty * sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  Params pp = p;
+  int a_ntx = ntx, a_nty = nty, a_sw = sweeps;
+  void *args[] = {&pp, &ex0, &ex1, &flags, &a_ntx, &a_nty, &a_sw};
+  e = cudaLaunchCooperativeKernel((const void *)kern, dim3((unsigned)(ntx * nty)), dim3(R::NT), args, R::SMEM, st);
+  note_launch();
+  return e;
+}
+
+template <int FORM, bool UNIT, int DIV>
+static cudaError_t launch_resident(const Params &p, double *ws, int sweeps, cudaStream_t st) {
+  int coop = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess || !coop)
+    return cudaErrorNotSupported;
+  cudaError_t e = cudaErrorNotSupported;
+  [&]<int... Ms>(std::integer_sequence<int, Ms...>) {
+    // M = MAXM, MAXM-1, ..., 1: first that fits
+    ((e == cudaErrorNotSupported ? (e = launch_resident_m<FORM, UNIT, DIV, ResGeo::MAXM - Ms>(p, ws, sweeps, st))
+                                 : e),
+     ...);
+  }(std::make_integer_sequence<int, ResGeo::MAXM>{});
+  return e;
+}
+
 // K4: 2D grids small enough to be L2-resident run M sweeps per pass in
 // shared-memory tiles (one wave of 1024-thread CTAs).
 static bool block2d_preferred(const KernelKey &key, const Params &p) {
@@ -675,11 +735,23 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
   if (!fused_supported(key, p)) return cudaSuccess;
   const size_t need = fused_workspace_bytes(key, p);
   if (!workspace || workspace_bytes < need || ((uintptr_t)workspace & 15)) return cudaSuccess;
+  // the grid itself (the workspace may be larger: K6 keeps its exchange grids there)
+  const size_t grid_bytes = (size_t)((p.nx + 2) * (p.ny + 2) * (shape_dim(key.shape) == 3 ? (p.nz + 2) : 1)) * sizeof(double);
   *handled = 1;
   // passes alternate u -> ws -> u ...; an odd count ends with one copy back
   double *bufs[2] = {p.u, workspace};
   int cur = 0;
   cudaError_t e = cudaSuccess;
+  if (!stream_only && resident_candidate(key, p) && workspace_bytes >= need) {
+    cudaError_t er = dispatch_fused(key, [&]<int S, int F, bool U, int D>() -> cudaError_t {
+      if constexpr (S == FD5 && U && D == DIV_POW2)
+        return launch_resident<F, U, D>(p, workspace, sweeps, st);
+      else
+        return cudaErrorNotSupported;
+    });
+    if (er != cudaErrorNotSupported) return er;
+    cudaGetLastError();   // clear the (non-sticky) not-supported status
+  }
   if (!stream_only && block2d_preferred(key, p)) {
     // FD5: 4 sweeps per pass, FE9: 2 (ghost 8 columns); remainder 1 at a time
     // (8 FD5 sweeps per pass measured slower: ghost and phase count outgrow the saved passes)
@@ -700,7 +772,7 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
       cur ^= 1;
     }
     if (e == cudaSuccess && cur == 1) {
-      e = cudaMemcpyAsync(p.u, workspace, need, cudaMemcpyDeviceToDevice, st);
+      e = cudaMemcpyAsync(p.u, workspace, grid_bytes, cudaMemcpyDeviceToDevice, st);
       note_launch();
     }
     return e;
@@ -743,7 +815,7 @@ cudaError_t launch_fused(const KernelKey &key, const Params &p, int sweeps, doub
     cur ^= 1;
   }
   if (e == cudaSuccess && cur == 1) {
-    e = cudaMemcpyAsync(p.u, workspace, need, cudaMemcpyDeviceToDevice, st);
+    e = cudaMemcpyAsync(p.u, workspace, grid_bytes, cudaMemcpyDeviceToDevice, st);
     note_launch();
   }
   return e;

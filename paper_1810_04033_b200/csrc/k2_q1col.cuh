@@ -166,8 +166,8 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
   unsigned ownbits = 0, fokbits = 0;
   const int64_t rowoff0 = (int64_t)(gy0 + r0) * p.sy + gx;   // row r0 of this thread
   const int sy32 = (int)p.sy;
-#pragma unroll
   unsigned inbits = 0;   // interior (updated) points: bit 2*a + s
+#pragma unroll
   for (int a = 0; a < RT; ++a) {
     const int r = r0 + a, gy = gy0 + r;
     ownbits |= (colown && r >= G::GY && r < G::GY + TYo) ? (1u << a) : 0u;

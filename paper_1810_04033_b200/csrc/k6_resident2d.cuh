@@ -1,0 +1,275 @@
+// k6_resident2d.cuh — K6: red-black 2D grids resident on chip for every sweep
+// (BASELINE config 1: FD5 1026^2, 100 sweeps).
+//
+// The whole grid is split into one tile per SM (cooperative launch: every
+// tile is co-resident).  A CTA keeps its tile's u in registers and f in
+// shared memory for the whole call, so u and f cross the chip boundary once
+// per call instead of once per pass (K4, k4_block2d.cuh, reloads its tile
+// from L2 every pass of M sweeps).  Sweeps run in rounds of M: a tile carries
+// a ghost ring of G = 2M cells (one per colour phase, plan.cuh's FD5 need),
+// runs the round's 2M colour phases locally — exact on the owned part, the
+// ring decays by one cell per phase — then publishes its owned part to an
+// exchange grid in global memory (L2), signals a per-tile flag and, once its
+// eight neighbours have signalled, reloads its ring from there.  Exchange
+// grids alternate per round, so a tile never overwrites data a slower
+// neighbour has yet to read (it waits for that neighbour's next flag first).
+//
+// Thread (warp w, lane i) owns tile rows 6w .. 6w+5, columns 4i .. 4i+3: the
+// colour of every one of its points is compile-time (tile origin chosen with
+// gx0 + gy0 even), x+-1 neighbours come from its own registers or one warp
+// shuffle, y+-1 from its own rows or the neighbouring warp's boundary row in
+// shared memory (double-buffered by phase: one block barrier per phase).
+// Arithmetic: common.cuh's acc_* in the canonical FD5 order, so the result is
+// bitwise identical to the per-colour kernel and the oracle.
+#pragma once
+#include "plan.cuh"
+
+namespace sl {
+
+struct ResGeo {
+  static constexpr int NW = 16;            // warps per CTA
+  static constexpr int NT = 32 * NW;       // 512 threads
+  static constexpr int RT = 6;             // rows per thread
+  static constexpr int CT = 4;             // columns per thread
+  static constexpr int TW = 32 * CT;       // tile width incl. ghost (128)
+  static constexpr int TH = NW * RT;       // tile height incl. ghost and the parity row (96)
+  static constexpr int FSM = TH * 2 * 32;  // f: [row][x parity][lane] double2
+  static constexpr int BSM = 2 * NW * 2 * TW;  // boundary rows: [buffer][warp][top, bottom][col]
+  static constexpr size_t SMEM = size_t(2 * FSM + BSM) * sizeof(double);
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+  static constexpr int MAXM = 5;
+  // owned extent per tile for M sweeps per round
+  static constexpr int own_w(int m) { return TW - 4 * m; }
+  static constexpr int own_h(int m) { return TH - 4 * m - 1; }
+};
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int FORM, bool UNIT, int DIV, int M, bool EDGE>
+__device__ __forceinline__ void k6_body(const Params &p, double *__restrict__ ex0, double *__restrict__ ex1,
+                                        int *__restrict__ flags, int ntx, int nty, int sweeps) {
+  using R = ResGeo;
+  constexpr int G = 2 * M, RT = R::RT, CT = R::CT, NW = R::NW;
+  extern __shared__ __align__(16) double rsm[];
+  double2 *fsm = reinterpret_cast<double2 *>(rsm);
+  double *bnd = rsm + 2 * R::FSM;
+
+  const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2;
+  const int nx = (int)p.nx, ny = (int)p.ny;
+  const int tile = blockIdx.x, tx = tile % ntx, ty = tile / ntx;
+  const int x0 = 2 * ((tx * (Sx / 2)) / ntx), x1 = 2 * (((tx + 1) * (Sx / 2)) / ntx);
+  const int y0 = (ty * Sy) / nty, y1 = ((ty + 1) * Sy) / nty;
+  const int gx0 = x0 - G;                           // even
+  const int delta = (gx0 + y0 - G) & 1;             // gx0 + gy0 even: colour = (lx + ly) & 1
+  const int gy0 = y0 - G - delta;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lx0 = CT * lane, ly0 = RT * warp;
+  const int64_t sy = p.sy;
+
+  // per-thread masks (bit r*CT + c): inside the grid array, interior (updated), owned
+  unsigned ingrid = 0, inter = 0, own = 0;
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+#pragma unroll
+    for (int c = 0; c < CT; ++c) {
+      const int gx = gx0 + lx0 + c, gy = gy0 + ly0 + r;
+      const unsigned b = 1u << (r * CT + c);
+      ingrid |= (gx >= 0 && gx < Sx && gy >= 0 && gy < Sy) ? b : 0u;
+      inter |= (gx >= 1 && gx <= nx && gy >= 1 && gy <= ny) ? b : 0u;
+      own |= (gx >= x0 && gx < x1 && gy >= y0 && gy < y1) ? b : 0u;
+    }
+  const double *gbase = p.u + (int64_t)(gy0 + ly0) * sy + gx0 + lx0;   // row ly0 of this thread
+
+  // ---- load: u into registers, f into shared memory (by x parity) ----
+  double U[RT][CT];
+#pragma unroll
+  for (int r = 0; r < RT; ++r) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const unsigned b = 3u << (r * CT + 2 * h);
+      double2 u2 = make_double2(0.0, 0.0), f2 = make_double2(0.0, 0.0);
+      if ((ingrid & b) == b) {
+        u2 = __ldcg(reinterpret_cast<const double2 *>(gbase + r * sy + 2 * h));
+        if (FORM == 1) f2 = __ldg(reinterpret_cast<const double2 *>(p.f + (gbase - p.u) + r * sy + 2 * h));
+      }
+      U[r][2 * h] = u2.x;
+      U[r][2 * h + 1] = u2.y;
+      if (FORM == 1) {
+        // parity 0 = columns 0, 2 of the lane; parity 1 = columns 1, 3
+        double *fp = reinterpret_cast<double *>(fsm);
+        fp[(((ly0 + r) * 2 + 0) * 32 + lane) * 2 + h] = f2.x;
+        fp[(((ly0 + r) * 2 + 1) * 32 + lane) * 2 + h] = f2.y;
+      }
+    }
+  }
+  auto publish = [&](int buf) {
+    double *top = bnd + ((buf * NW + warp) * 2 + 0) * R::TW + lx0;
+    double *bot = bnd + ((buf * NW + warp) * 2 + 1) * R::TW + lx0;
+    reinterpret_cast<double2 *>(top)[0] = make_double2(U[0][0], U[0][1]);
+    reinterpret_cast<double2 *>(top)[1] = make_double2(U[0][2], U[0][3]);
+    reinterpret_cast<double2 *>(bot)[0] = make_double2(U[RT - 1][0], U[RT - 1][1]);
+    reinterpret_cast<double2 *>(bot)[1] = make_double2(U[RT - 1][2], U[RT - 1][3]);
+  };
+  int pb = 0;                 // boundary-row buffer holding the current state
+  publish(pb);
+  __syncthreads();
+  if (threadIdx.x == 0) {     // loaded: neighbours may now overwrite u (the final stores)
+    __threadfence();
+    st_release_gpu(flags + tile, 1);
+  }
+  // a neighbour that never signals (a bug, or a launch that is not co-resident)
+  // must not hang the device: after 2 s the wait gives up and flags status bit 1
+  auto wait_neighbours = [&](int want) {
+    if (threadIdx.x == 0) {
+      const uint64_t t0 = globaltimer_ns();
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const int nxt = tx + dx, nyt = ty + dy;
+          if ((dx || dy) && nxt >= 0 && nxt < ntx && nyt >= 0 && nyt < nty)
+            while (ld_acquire_gpu(flags + nyt * ntx + nxt) < want) {
+              __nanosleep(32);
+              if (globaltimer_ns() - t0 > 2000000000ull) {
+                atomicOr(p.status, 2);
+                break;
+              }
+            }
+        }
+      __threadfence();
+    }
+    __syncthreads();
+  };
+
+  const int rounds = (sweeps + M - 1) / M;
+  for (int rnd = 0; rnd < rounds; ++rnd) {
+    const int m = rnd == rounds - 1 ? sweeps - (rounds - 1) * M : M;
+    const int kstart = 2 * (M - m);          // a short last round runs the round's last 2m phases
+    [&]<int... Ks>(std::integer_sequence<int, Ks...>) {
+      (
+          [&] {
+            constexpr int K = Ks, C = K & 1;
+            if (K < kstart) return;          // CTA-uniform
+            const double *above = bnd + ((pb * NW + (warp > 0 ? warp - 1 : warp)) * 2 + 1) * R::TW + lx0;
+            const double *below = bnd + ((pb * NW + (warp < NW - 1 ? warp + 1 : warp)) * 2 + 0) * R::TW + lx0;
+            double out[RT][2];
+#pragma unroll
+            for (int r = 0; r < RT; ++r) {
+              constexpr int dummy = 0;
+              (void)dummy;
+              const int c1 = (C + r) & 1;    // compile-time after unrolling
+              const double2 fv = FORM == 1 ? fsm[((ly0 + r) * 2 + c1) * 32 + lane] : make_double2(0.0, 0.0);
+              // the neighbour column across the lane boundary (other colour: unchanged this phase)
+              const double xl = __shfl_up_sync(0xffffffffu, U[r][CT - 1], 1);
+              const double xr = __shfl_down_sync(0xffffffffu, U[r][0], 1);
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int c = c1 + 2 * j;
+                const double uc = U[r][c];
+                const double up = r > 0 ? U[r - 1][c] : above[c];
+                const double dn = r < RT - 1 ? U[r + 1][c] : below[c];
+                const double lf = c > 0 ? U[r][c - 1] : xl;
+                const double rt = c < CT - 1 ? U[r][c + 1] : xr;
+                double acc = acc_init<FORM, UNIT>(uc, p);
+                acc = acc_add<FORM, UNIT>(acc, up, 0, p);   // (0,-1)
+                acc = acc_add<FORM, UNIT>(acc, lf, 1, p);   // (-1,0)
+                acc = acc_add<FORM, UNIT>(acc, rt, 2, p);   // (1,0)
+                acc = acc_add<FORM, UNIT>(acc, dn, 3, p);   // (0,1)
+                out[r][j] = acc_finish<FORM, UNIT, DIV>(acc, uc, j == 0 ? fv.x : fv.y, p);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < RT; ++r)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int c = ((C + r) & 1) + 2 * j;
+                if (!EDGE || ((inter >> (r * CT + c)) & 1u)) U[r][c] = out[r][j];
+              }
+            pb ^= 1;
+            publish(pb);
+            __syncthreads();
+          }(),
+          ...);
+    }(std::make_integer_sequence<int, 2 * M>{});
+
+    if (rnd == rounds - 1) break;
+    // ---- exchange: owned part -> exchange grid, flag, neighbours' parts -> ring ----
+    double *ex = (rnd & 1) ? ex1 : ex0;
+    double *eb = ex + (gbase - p.u);
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (((own >> (r * CT + 2 * h)) & 3u) == 3u)
+          stg_pair(eb + r * sy + 2 * h, U[r][2 * h], U[r][2 * h + 1]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release_gpu(flags + tile, rnd + 2);
+    }
+    wait_neighbours(rnd + 2);
+#pragma unroll
+    for (int r = 0; r < RT; ++r)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const unsigned b = 3u << (r * CT + 2 * h);
+        if ((own & b) == 0u && (ingrid & b) == b) {
+          const double2 v = __ldcg(reinterpret_cast<const double2 *>(eb + r * sy + 2 * h));
+          U[r][2 * h] = v.x;
+          U[r][2 * h + 1] = v.y;
+        }
+      }
+    publish(pb);
+    __syncthreads();
+  }
+
+  // ---- owned part -> u (every neighbour has loaded its ring from u by now) ----
+  wait_neighbours(1);
+  unsigned emax = 0;
+  double *ub = p.u + (gbase - p.u);
+#pragma unroll
+  for (int r = 0; r < RT; ++r)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (((own >> (r * CT + 2 * h)) & 3u) == 3u) {
+        stg_pair(ub + r * sy + 2 * h, U[r][2 * h], U[r][2 * h + 1]);
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const unsigned ex = (unsigned)__double2hiint(U[r][2 * h + s]) & 0x7ff00000u;
+          emax = max(emax, ((inter >> (r * CT + 2 * h + s)) & 1u) ? ex : 0u);
+        }
+      }
+  if (__any_sync(0xffffffffu, emax == 0x7ff00000u) && lane == 0) atomicOr(p.status, 1);
+}
+
+template <int FORM, bool UNIT, int DIV, int M>
+__global__ void __launch_bounds__(ResGeo::NT, 1)
+k6_resident2d(Params p, double *ex0, double *ex1, int *flags, int ntx, int nty, int sweeps) {
+  constexpr int G = 2 * M;
+  const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2;
+  const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
+  const int x0 = 2 * ((tx * (Sx / 2)) / ntx);
+  const int y0 = (ty * Sy) / nty;
+  const int gy0 = y0 - G - ((x0 + y0) & 1);
+  // interior tile: every point of the window is an interior grid point
+  const bool edge = x0 - G < 1 || x0 - G + ResGeo::TW > (int)p.nx + 1 || gy0 < 1 ||
+                    gy0 + ResGeo::TH > (int)p.ny + 1;
+  if (edge)
+    k6_body<FORM, UNIT, DIV, M, true>(p, ex0, ex1, flags, ntx, nty, sweeps);
+  else
+    k6_body<FORM, UNIT, DIV, M, false>(p, ex0, ex1, flags, ntx, nty, sweeps);
+}
+
+}  // namespace sl

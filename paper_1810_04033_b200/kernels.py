@@ -36,6 +36,18 @@ class NumericsError(ArithmeticError):
     """A cell update produced a non-finite value (reference kernels.py:38-39)."""
 
 
+class ExchangeTimeout(RuntimeError):
+    """A resident (cooperative) sweep kernel gave up waiting for a neighbouring
+    tile's exchange flag (status bit 1): the result is not valid."""
+
+
+def status_error(flag: int, what: str) -> Exception:
+    """The exception a non-zero device status word stands for."""
+    if flag & 2:
+        return ExchangeTimeout(f"tile exchange timed out during {what}")
+    return NumericsError(f"non-finite update during {what}")
+
+
 def _canonical(offsets):
     # outer axis slowest: sort by reversed displacement so x varies fastest
     return tuple(sorted(offsets, key=lambda off: tuple(reversed(off))))
@@ -247,7 +259,7 @@ class DeviceCall:
         flag = int(self.status.item())
         if flag:
             self.status.zero_()
-            raise NumericsError(f"non-finite update during {what}")
+            raise status_error(flag, what)
 
 
 def _call(mesh: Mesh, kind: StencilKind) -> DeviceCall:

@@ -19,7 +19,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _native
-from .kernels import NumericsError, StencilKind
+from .kernels import NumericsError, StencilKind, status_error
 
 __all__ = ["SweepPipeline"]
 
@@ -109,9 +109,11 @@ class SweepPipeline:
         """Wait for every queued job; NumericsError if any update was non-finite."""
         for s in self._in_flight:
             s["free"].synchronize()
-        bad = any(int(s["status"].item()) for s in self._slots)
+        bad = 0
+        for s in self._slots:
+            bad |= int(s["status"].item())
         for s in self._slots:
             s["status"].zero_()
         self._in_flight = []
         if bad:
-            raise NumericsError("non-finite update in a pipelined sweep")
+            raise status_error(bad, "a pipelined sweep")
