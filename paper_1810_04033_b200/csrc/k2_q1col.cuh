@@ -16,7 +16,8 @@
 // a chunk of z; 12 warps.  Thread (warp w, lane i) owns column pair (2i, 2i+1)
 // of the RT = 4 tile rows r0 = 4w + delta .. r0 + 3, where delta makes row r0
 // a y-parity 0 row, so each group updates 2 x 2 points of the thread (rows A,
-// A + 2).  The thread keeps its rows of planes p-2 .. p in a register ring
+// A + 2).  (The geometry is a set of build-time constants, Q1Geo below: CPL
+// columns per lane, LX lanes along x and 32/LX lane rows per warp.)  The thread keeps its rows of planes p-2 .. p in a register ring
 // (plane p+1, read only by G0/G1, comes from its slot); otherwise only the
 // row of the warp above/below comes from the plane's shared-memory slot, and
 // the x+-1 columns from warp shuffles.  Neighbour values enter the sums as
@@ -25,9 +26,10 @@
 // slot for the neighbouring warps.
 //
 // u planes arrive by TMA (64 x 49 x 1 boxes, zero-filled out of range) into
-// 8 smem slots, up to six planes ahead.  The loop is unrolled by two pair
-// steps (one ring turn), so ring indices are compile-time; slot offsets and
-// mbarrier parities are cheap runtime values.  Out-of-range groups and ghost
+// 8 smem slots, up to six planes ahead.  One pair step per loop iteration:
+// the ring entries have fixed roles (planes pp-2, pp-1, pp) and plane pp moves
+// to entry 0 at the end of the step; slot offsets and mbarrier parities are
+// cheap runtime values.  Out-of-range groups and ghost
 // points are computed and masked (no branches around the shuffles: skipping
 // the groups a warp has no used point in measured 0.7 % slower, the early exit
 // grows the unrolled loop by 60 %); the exact
@@ -44,25 +46,57 @@ namespace sl {
 // must not bloat the unrolled loop (instruction-cache pressure).
 static __device__ __noinline__ double q1_div_exact(double a, double b) { return __ddiv_rn(a, b); }
 
-struct Q1Geo {
-  static constexpr FPlan P = make_plan(Q1, 8, 1, false);
-  static constexpr int GX = 4, GY = 4, GZ = 2;            // plan load margins
-  static constexpr int PX = 64, PY = 48;                  // tile incl. ghost
-  static constexpr int BOXY = PY + 1;                     // rows loaded (delta shift)
-  static constexpr int TX = PX - 2 * GX, TY = PY - 2 * GY;
-  static constexpr int S = 8;                             // smem slots
-  static constexpr int RR = 4;                            // ring entries (planes p-2 .. p live)
+// Build-time geometry (A/B switches).  Default: a lane owns a column pair
+// (CPL = 2), a warp is 32 lanes along x, 12 warps cover a 64 x 48 tile (384
+// threads, 168 registers, 8 plane slots).  Measured alternatives on config 4
+// (all bitwise equal, all slower than the default's 140 GLUP/s):
+//   -DQ1_CPL=4 -DQ1_LX=16 -DQ1_PY=64 -DQ1_S=6 -DQ1_SHIFT=1   lanes own four
+//     columns (half the shuffles per point), warps are 16 x 2 lanes, 8 warps
+//     cover 64 x 64 (256 threads, 255 registers): 125 GLUP/s, 127 with
+//     -DQ1_NOSWAP (2-way LDS/STS.128 bank conflicts instead of register swaps);
+//   the same with -DQ1_RT=2 (16 warps, 128 registers): 118 GLUP/s.
+#ifndef Q1_CPL
+#define Q1_CPL 2
+#endif
+#ifndef Q1_LX
+#define Q1_LX 32
+#endif
+#ifndef Q1_PY
+#define Q1_PY 48
+#endif
+#ifndef Q1_S
+#define Q1_S 8
+#endif
 #ifndef Q1_RT
 #define Q1_RT 4
 #endif
+// Q1_SHIFT = 1: the loaded window starts on a y-parity-0 row (its origin moves
+// up by the tile's parity offset delta), so PY rows are loaded instead of
+// PY + 1 and a tile owns at most PY - 2 GY - 1 rows.
+#ifndef Q1_SHIFT
+#define Q1_SHIFT 0
+#endif
+struct Q1Geo {
+  static constexpr FPlan P = make_plan(Q1, 8, 1, false);
+  static constexpr int GX = 4, GY = 4, GZ = 2;            // plan load margins
+  static constexpr int CPL = Q1_CPL;                      // columns per lane
+  static constexpr int LX = Q1_LX, LY = 32 / LX;          // lanes along x / lane rows per warp
+  static constexpr int PX = CPL * LX, PY = Q1_PY;         // tile incl. ghost
+  static constexpr bool SHIFT = Q1_SHIFT != 0;
+  static constexpr int BOXY = SHIFT ? PY : PY + 1;        // rows loaded
+  static constexpr int TX = PX - 2 * GX, TY = PY - 2 * GY - (SHIFT ? 1 : 0);
+  static constexpr int S = Q1_S;                          // smem slots (4 live planes + S - 4 ahead)
+  static constexpr int RR = 4;                            // ring entries (planes p-2 .. p live)
   static constexpr int RT = Q1_RT;                        // tile rows per thread
-  static constexpr int NT = 32 * PY / RT;                 // 384
+  static constexpr int NT = 32 * PY / (RT * LY);
   static constexpr int LAGMAX = 1;
   static constexpr int SLOTE = PX * BOXY;
   static constexpr int LEADE = 2 * PX;                    // guard rows before slot 0
-  static constexpr int FBUFE = 2 * (RT / 2) * 2 * NT;      // f staging: 2 buffers x H rows x 2 cols
+  static constexpr int FBUFE = 2 * (RT / 2) * CPL * NT;   // f staging: 2 buffers x H rows x PX cols per lane row
   static constexpr size_t SMEM = size_t(LEADE + S * SLOTE + 2 * PX + FBUFE) * sizeof(double) + S * 8;
   static_assert(P.load[0] <= GX && P.load[1] <= GY && P.load[2] <= GZ, "ghost margin");
+  static_assert(CPL % 2 == 0 && LX * LY == 32 && PY % (RT * LY) == 0 && S >= 6 && (S & 1) == 0, "geometry");
+  static_assert(4 * (RT / 2) * CPL <= 32 && RT * CPL <= 32, "mask bits");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 
@@ -83,10 +117,12 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
                                            int64_t ntx, int64_t nty, int64_t nzc) {
   using G = Q1Geo;
   constexpr FPlan P = G::P;
-  constexpr int RT = G::RT, H = RT / 2, RR = G::RR;
+  constexpr int RT = G::RT, H = RT / 2, C = G::CPL, CP = C / 2;
+  constexpr int RR = 3;   // ring entries: planes pp-2, pp-1, pp
+  static_assert(CP == 1 || CP == 2, "columns per lane");
   extern __shared__ __align__(128) double qsm[];
   double *su = qsm + G::LEADE;  // slot k at su + k*SLOTE
-  double *fbuf = su + G::S * G::SLOTE + 2 * G::PX;   // [buffer][h][thread] double2
+  double *fbuf = su + G::S * G::SLOTE + 2 * G::PX;   // [lane row][h][PX]
   uint64_t *mb = reinterpret_cast<uint64_t *>(fbuf + G::FBUFE);
   const uint32_t su_s = (uint32_t)__cvta_generic_to_shared(su);
   const uint32_t mb_s = (uint32_t)__cvta_generic_to_shared(mb);
@@ -100,11 +136,16 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
   const int zlen = p.zhi - p.zlo;
   const int z0 = p.zlo + (int)(((int64_t)zc * zlen) / nzc), z1 = p.zlo + (int)(((int64_t)(zc + 1) * zlen) / nzc);
   const int TXo = x1 - x0, TYo = y1 - y0;
-  const int gx0 = x0 - G::GX, gy0 = y0 - G::GY;
+  const int gx0 = x0 - G::GX;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gx = gx0 + 2 * lane;
-  const int delta = (1 - p.py - gy0) & 1;        // local row r0 has y parity 0
-  const int r0 = RT * warp + delta;              // this thread's rows r0 (qy 0) .. r0 + RT - 1
+  const int lx = lane % G::LX;                   // lane along x: columns C*lx .. C*lx + C - 1
+  const int vrow = warp * G::LY + lane / G::LX;  // band of RT rows
+  const int gx = gx0 + C * lx;
+  // local row r0 has y parity 0; the tile's first owned row is local row TM
+  const int delta = (1 - p.py - (y0 - G::GY)) & 1;
+  const int gy0 = G::SHIFT ? y0 - G::GY - delta : y0 - G::GY;
+  const int TM = G::SHIFT ? G::GY + delta : G::GY;
+  const int r0 = G::SHIFT ? RT * vrow : RT * vrow + delta;   // this thread's rows r0 (qy 0) .. r0 + RT - 1
   const int64_t sz = p.sz;
 
   // pair steps at planes pp = p_begin, p_begin + 2, ... of parity qz = 0;
@@ -120,28 +161,62 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
   const int zlim = z1 + G::GZ;
   const int base = p_begin - 2;                  // plane held by slot 0 / ring 0 in use 0
 
+  auto slot_idx = [&](int plane) -> int { return (int)((unsigned)(plane - base) % (unsigned)G::S); };
   auto issue = [&](int plane) {
-    const int sl = (plane - base) & (G::S - 1);
+    const int sl = slot_idx(plane);
     const uint32_t bar = mb_s + 8u * sl;
     const bool live = plane >= 0 && plane < Sz && plane < zlim;
     mbar_expect3(bar, live ? (uint32_t)(G::SLOTE * 8) : 0u);
     if (live) tma_load_3d(su_s + sl * G::SLOTE * 8, &tmu, gx0, gy0, plane, bar);
   };
   auto wait_plane = [&](int plane) {
-    mbar_wait3(mb_s + 8u * (uint32_t)((plane - base) & (G::S - 1)), (uint32_t)(((plane - base) >> 3) & 1));
+    mbar_wait3(mb_s + 8u * (uint32_t)slot_idx(plane), ((unsigned)(plane - base) / (unsigned)G::S) & 1u);
   };
-  double *me = su + r0 * G::PX + 2 * lane;  // (slot 0, row r0, col 2*lane)
-  auto slot_of = [&](int plane) -> double * { return me + ((plane - base) & (G::S - 1)) * G::SLOTE; };
+  // A lane's C = 4 columns are two 16-byte pairs, 32 bytes from the next
+  // lane's: eight lanes all accessing "pair 0" would use only every other
+  // 16-byte bank group (a 2-way conflict on every LDS/STS.128).  Lanes 4..7 of
+  // every eight therefore access their pairs in the opposite order (qsw) and
+  // swap in registers: first access at element qa, second at qb.
+#ifdef Q1_NOSWAP
+  const bool qsw = false;
+#else
+  const bool qsw = CP == 2 && ((lx >> 2) & 1);
+#endif
+  const int qa = qsw ? 2 : 0, qb = CP == 2 ? 2 - qa : 0;
+  double *me = su + r0 * G::PX + C * lx;  // (slot 0, row r0, first column of the lane)
+  auto slot_of = [&](int plane) -> double * { return me + slot_idx(plane) * G::SLOTE; };
+  auto ld_row = [&](const double *row, double (&v)[C]) {   // row: the lane's first column
+    if constexpr (CP == 1) {
+      const double2 m = *reinterpret_cast<const double2 *>(row);
+      v[0] = m.x;
+      v[1] = m.y;
+    } else {
+      const double2 a = *reinterpret_cast<const double2 *>(row + qa);
+      const double2 b = *reinterpret_cast<const double2 *>(row + qb);
+      v[0] = qsw ? b.x : a.x;
+      v[1] = qsw ? b.y : a.y;
+      v[2] = qsw ? a.x : b.x;
+      v[3] = qsw ? a.y : b.y;
+    }
+  };
+  auto st_row = [&](double *row, const double (&v)[C]) {
+    if constexpr (CP == 1) {
+      *reinterpret_cast<double2 *>(row) = make_double2(v[0], v[1]);
+    } else {
+      *reinterpret_cast<double2 *>(row + qa) = make_double2(qsw ? v[2] : v[0], qsw ? v[3] : v[1]);
+      *reinterpret_cast<double2 *>(row + qb) = make_double2(qsw ? v[0] : v[2], qsw ? v[1] : v[3]);
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < G::S; ++k) mbar_init3(mb_s + 8u * k);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int k = 0; k < 6; ++k) issue(base + k);  // planes p_begin-2 .. p_begin+3
+    for (int k = 0; k < G::S - 2; ++k) issue(base + k);  // planes p_begin-2 .. p_begin+S-5
   }
   __syncthreads();
 
   // ---- thread-constant masks ------------------------------------------------
-  // ok bit (4*gi + 2*h + s): point s of the h-th row (A + 2h) of group gi
+  // ok bit ((gi*H + h)*C + s): point s of the h-th row (A + 2h) of group gi
   // (colours 2gi, 2gi+1) is inside its need region and the grid interior (x, y)
   unsigned okbits = 0;
 #pragma unroll
@@ -152,76 +227,87 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       const int r = r0 + A + 2 * h, gy = gy0 + r;
-      const bool rok = r >= G::GY - nyj && r < G::GY + TYo + nyj && gy >= 1 && gy <= ny;
+      const bool rok = r >= TM - nyj && r < TM + TYo + nyj && gy >= 1 && gy <= ny;
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int lx = 2 * lane + s;
-        const bool cok = lx >= G::GX - nxj && lx < G::GX + TXo + nxj && gx + s >= 1 && gx + s <= nx;
-        okbits |= (rok && cok) ? (1u << (4 * gi + 2 * h + s)) : 0u;
+      for (int s = 0; s < C; ++s) {
+        const int lc = C * lx + s;
+        const bool cok = lc >= G::GX - nxj && lc < G::GX + TXo + nxj && gx + s >= 1 && gx + s <= nx;
+        okbits |= (rok && cok) ? (1u << ((gi * H + h) * C + s)) : 0u;
       }
     }
   }
-  // owned output rows (the tiles partition [0, S) in x and y)
-  const bool colown = 2 * lane >= G::GX && 2 * lane < G::GX + TXo;
+  // owned output rows and column pairs (the tiles partition [0, S) in x and
+  // y; tile starts are even, so a pair is owned as a whole): bit a*CP + pair
   unsigned ownbits = 0, fokbits = 0;
   const int64_t rowoff0 = (int64_t)(gy0 + r0) * p.sy + gx;   // row r0 of this thread
   const int sy32 = (int)p.sy;
-  unsigned inbits = 0;   // interior (updated) points: bit 2*a + s
+  unsigned inbits = 0;   // interior (updated) points: bit C*a + s
 #pragma unroll
   for (int a = 0; a < RT; ++a) {
     const int r = r0 + a, gy = gy0 + r;
-    ownbits |= (colown && r >= G::GY && r < G::GY + TYo) ? (1u << a) : 0u;
-    fokbits |= (gy >= 0 && gy < Sy && gx >= 0 && gx + 1 < Sx) ? (1u << a) : 0u;
 #pragma unroll
-    for (int s = 0; s < 2; ++s)
-      inbits |= (gy >= 1 && gy <= ny && gx + s >= 1 && gx + s <= nx) ? (1u << (2 * a + s)) : 0u;
+    for (int pr = 0; pr < CP; ++pr) {
+      const int lc = C * lx + 2 * pr;
+      const bool colown = lc >= G::GX && lc < G::GX + TXo;
+      ownbits |= (colown && r >= TM && r < TM + TYo) ? (1u << (a * CP + pr)) : 0u;
+      // f is staged by 16-byte chunks of the lane row's PX columns: this lane copies chunks lx + LX*pr
+      const int fc = gx0 + 2 * (lx + G::LX * pr);
+      fokbits |= (gy >= 0 && gy < Sy && fc >= 0 && fc + 1 < Sx) ? (1u << (a * CP + pr)) : 0u;
+    }
+#pragma unroll
+    for (int s = 0; s < C; ++s)
+      inbits |= (gy >= 1 && gy <= ny && gx + s >= 1 && gx + s <= nx) ? (1u << (C * a + s)) : 0u;
   }
 
-  // own rows of planes pp-2 .. pp+1: [row][ring][col]; plane P at (P - base) % RR
-  double U[RT][RR][2];
+  // own rows of planes pp-2, pp-1, pp: [row][ring entry][col] (plane pp+1, read
+  // only by G0/G1, comes from its slot).  Entry 0 survives a pair step (it is
+  // the previous step's plane pp), entries 1 and 2 are loaded at its start.
+  double U[RT][RR][C];
   wait_plane(base);
   wait_plane(base + 1);
+  {
+    const double *pl = slot_of(base);
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const double *pl = slot_of(base + k);
-#pragma unroll
-    for (int a = 0; a < RT; ++a) {
-      const double2 v = *reinterpret_cast<const double2 *>(pl + a * G::PX);
-      U[a][k][0] = v.x;
-      U[a][k][1] = v.y;
-    }
+    for (int a = 0; a < RT; ++a) ld_row(pl + a * G::PX, U[a][0]);
   }
-#pragma unroll
-  for (int a = 0; a < RT; ++a)
-#pragma unroll
-    for (int k = 2; k < RR; ++k) U[a][k][0] = U[a][k][1] = 0.0;
 
-  // f of group gi at plane pz (rows A + 2h)
-  // f rows of group gi at plane pz (rows A + 2h) are staged per thread in
-  // shared memory by cp.async, one group ahead of their use, alternating
-  // between two buffers (the groups of a pair step use buffers 0, 1, 0, 1).
-  // cp.async.wait_group waits for exactly the older copies, so the newest
-  // copy in flight never delays a consumer (a register LDG would share its
-  // scoreboard with it).  Masked rows are zero-filled (src size 0).
-  const double *fthr = p.f + rowoff0;
-  const uint32_t fb_s = (uint32_t)__cvta_generic_to_shared(fbuf) + 16u * threadIdx.x;
+  // f rows of group gi at plane pz (rows A + 2h) are staged per lane row (the
+  // LX lanes that share a band of rows) in shared memory by cp.async, one
+  // group ahead of their use, alternating between two buffers (the groups of
+  // a pair step use buffers 0, 1, 0, 1).  The lanes copy the row's PX columns
+  // as consecutive 16-byte chunks (coalesced: chunk lx + LX*j by lane lx) and
+  // each lane reads its own columns.  cp.async.wait_group 1 waits for exactly
+  // the older copy, so the newest one in flight never delays a consumer, and
+  // it does not matter where in the group the scheduler places the wait (a
+  // wait for a copy issued in the same group gets hoisted right behind it; a
+  // register LDG would share its scoreboard with the plane loads).  Masked
+  // chunks are zero-filled (src size 0).  __syncwarp orders the lanes' copies
+  // and reads.
+  const double *fthr = p.f + (int64_t)(gy0 + r0) * p.sy + gx0 + 2 * lx;
+  double *frow = fbuf + vrow * (2 * H * G::PX);
+  const uint32_t fb_s = (uint32_t)__cvta_generic_to_shared(frow) + 16u * lx;
   auto issue_f = [&](int gi, int pz, int buf) {
     const int A = gi & 1;
     const bool zin = pz >= 0 && pz < Sz;
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const bool live = FORM == 1 && ((fokbits >> (A + 2 * h)) & 1u) && zin;
-      const double *fp = live ? fthr + (int64_t)pz * sz + (A + 2 * h) * sy32 : p.u;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(fb_s + 16u * (buf * H + h) * G::NT),
-                   "l"(fp), "r"(live ? 16 : 0));
-    }
-    asm volatile("cp.async.commit_group;");
-  };
-  auto read_f = [&](int buf, double2 (&fv)[H]) {
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();   // every lane has read this buffer's previous contents
 #pragma unroll
     for (int h = 0; h < H; ++h)
-      fv[h] = reinterpret_cast<const double2 *>(fbuf)[(buf * H + h) * G::NT + threadIdx.x];
+#pragma unroll
+      for (int pr = 0; pr < CP; ++pr) {
+        const bool live = FORM == 1 && ((fokbits >> ((A + 2 * h) * CP + pr)) & 1u) && zin;
+        const double *fp = live ? fthr + (int64_t)pz * sz + (A + 2 * h) * sy32 + 2 * G::LX * pr : p.u;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                         fb_s + 8u * ((buf * H + h) * G::PX + 2 * G::LX * pr)),
+                     "l"(fp), "r"(live ? 16 : 0)
+                     : "memory");
+      }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto read_f = [&](int buf, double (&fv)[H][C]) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();   // the other lanes' chunks have landed too
+#pragma unroll
+    for (int h = 0; h < H; ++h) ld_row(frow + (buf * H + h) * G::PX + C * lx, fv[h]);
   };
   if (FORM == 1) issue_f(0, p_begin, 0);
 
@@ -232,15 +318,12 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
 
   // one colour group GI at plane pz = pp - (GI >> 1); RP = ring entry of pp
   auto group = [&]<int GI, int RP>(int pp) {
-    // next group's right-hand side in flight, this group's from its buffer
-    double2 fv[H];
-    if (FORM == 1) {
-      constexpr int NGI = (GI + 1) & 3;
-      issue_f(NGI, GI == 0 ? pp : GI == 3 ? pp + 2 : pp - 1, NGI & 1);
-      read_f(GI & 1, fv);
-    }
     constexpr int A = GI & 1;                      // rows A, A + 2
     constexpr int LAGG = GI >> 1;
+    if (FORM == 1) {                               // next group's right-hand side in flight
+      constexpr int NGI = (GI + 1) & 3;
+      issue_f(NGI, GI == 0 ? pp : GI == 3 ? pp + 2 : pp - 1, NGI & 1);
+    }
     constexpr int RC = (RP - LAGG + RR) % RR;      // ring entry of plane pz
     constexpr int NZJ = cmax(P.need[2 * GI][2], P.need[2 * GI + 1][2]);
     const int pz = pp - LAGG;
@@ -251,11 +334,11 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     // convergence code)
     const bool pzin = pz >= 1 && pz <= nz;
     (void)NZJ;
-    double acc[H][2];
+    double acc[H][C];
 #pragma unroll
     for (int h = 0; h < H; ++h)
 #pragma unroll
-      for (int s = 0; s < 2; ++s) acc[h][s] = acc_init<FORM, UNIT>(U[A + 2 * h][RC][s], p);
+      for (int s = 0; s < C; ++s) acc[h][s] = acc_init<FORM, UNIT>(U[A + 2 * h][RC][s], p);
 #pragma unroll
     for (int dz = -1; dz <= 1; ++dz) {
       const int rs = (RC + dz + RR) % RR;
@@ -274,30 +357,28 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
         const int d = A - 1 + i;
         const bool odd = ((d - A) & 1) != 0;
         if (dz == 0 && !odd) continue;  // no in-plane face/centre rows
-        double lo, hi;
+        double v[C];
         if (d >= 0 && d < RT && !(LAGG == 0 && dz == 1)) {
-          lo = U[d][rs][0];
-          hi = U[d][rs][1];
+#pragma unroll
+          for (int s = 0; s < C; ++s) v[s] = U[d][rs][s];
         } else {
-          const double2 m = *reinterpret_cast<const double2 *>(pl + d * G::PX);
-          lo = m.x;
-          hi = m.y;
+          ld_row(pl + d * G::PX, v);
         }
-        double pe[4], pc[4];
-        pe[1] = UNIT ? lo : __dmul_rn(wE, lo);
-        pe[2] = UNIT ? hi : __dmul_rn(wE, hi);
+        // window columns -1 .. C (index + 1); the two outer ones come from the
+        // neighbouring lanes of the same lane row
+        double pe[C + 2], pc[C + 2];
+#pragma unroll
+        for (int s = 0; s < C; ++s) pe[s + 1] = UNIT ? v[s] : __dmul_rn(wE, v[s]);
         if (!UNIT && odd && dz != 0) {
-          pc[1] = __dmul_rn(wC, lo);
-          pc[2] = __dmul_rn(wC, hi);
-          pc[0] = __shfl_up_sync(0xffffffffu, pc[2], 1);
-          pc[3] = __shfl_down_sync(0xffffffffu, pc[1], 1);
+#pragma unroll
+          for (int s = 0; s < C; ++s) pc[s + 1] = __dmul_rn(wC, v[s]);
+          pc[0] = __shfl_up_sync(0xffffffffu, pc[C], 1, G::LX);
+          pc[C + 1] = __shfl_down_sync(0xffffffffu, pc[1], 1, G::LX);
         } else {
-          pe[0] = __shfl_up_sync(0xffffffffu, pe[2], 1);
-          pe[3] = __shfl_down_sync(0xffffffffu, pe[1], 1);
-          pc[0] = pe[0];
-          pc[1] = pe[1];
-          pc[2] = pe[2];
-          pc[3] = pe[3];
+          pe[0] = __shfl_up_sync(0xffffffffu, pe[C], 1, G::LX);
+          pe[C + 1] = __shfl_down_sync(0xffffffffu, pe[1], 1, G::LX);
+#pragma unroll
+          for (int s = 0; s < C + 2; ++s) pc[s] = pe[s];
         }
 #pragma unroll
         for (int h = 0; h < H; ++h) {
@@ -309,9 +390,9 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
             if (o.z != dz || o.y != oy) continue;
             const bool corner = o.x != 0 && o.y != 0 && o.z != 0;
 #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              const double v = corner ? pc[o.x + 1 + s] : pe[o.x + 1 + s];
-              acc[h][s] = (FORM == 1 && UNIT) ? __dsub_rn(acc[h][s], v) : __dadd_rn(acc[h][s], v);
+            for (int s = 0; s < C; ++s) {
+              const double t = corner ? pc[o.x + 1 + s] : pe[o.x + 1 + s];
+              acc[h][s] = (FORM == 1 && UNIT) ? __dsub_rn(acc[h][s], t) : __dadd_rn(acc[h][s], t);
             }
           }
         }
@@ -320,14 +401,16 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     // division by w_c.  The fast-path range test ignores the lane masks (a
     // zero-filled point outside the grid only sends its warp into the
     // fallback, which applies them), so no mask is kept live across it.
-    bool ok[H][2], slow = false;
-    double a[H][2], q[H][2];
+    double fv[H][C];
+    if (FORM == 1) read_f(GI & 1, fv);
+    bool ok[H][C], slow = false;
+    double a[H][C], q[H][C];
 #pragma unroll
     for (int h = 0; h < H; ++h)
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        ok[h][s] = !EDGE || ((okbits >> (4 * GI + 2 * h + s)) & 1u);
-        a[h][s] = FORM == 0 ? acc[h][s] : __dsub_rn(s == 0 ? fv[h].x : fv[h].y, acc[h][s]);
+      for (int s = 0; s < C; ++s) {
+        ok[h][s] = !EDGE || ((okbits >> ((GI * H + h) * C + s)) & 1u);
+        a[h][s] = FORM == 0 ? acc[h][s] : __dsub_rn(fv[h][s], acc[h][s]);
         if (DIV == DIV_RCP) {
           const double e = __dmul_rn(a[h][s], p.rwc);
           q[h][s] = __fma_rn(__fma_rn(-p.wc, e, a[h][s]), p.rwc, e);
@@ -343,18 +426,18 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
 #pragma unroll
       for (int h = 0; h < H; ++h)
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < C; ++s) {
           const unsigned xe = (unsigned)__double2hiint(a[h][s]) & 0x7ff00000u;
           if (ok[h][s] && (xe - (64u << 20)) >= (1919u << 20)) q[h][s] = q1_div_exact(a[h][s], p.wc);
         }
     }
     // commit: ring, publish to the plane's slot (a dropped plane gets its
     // unchanged values back from the slot)
-    double *pc = slot_of(pz);
+    double *pcs = slot_of(pz);
 #pragma unroll
     for (int h = 0; h < H; ++h) {
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < C; ++s) {
         const double uc = U[A + 2 * h][RC][s];
         const double out = FORM == 0 ? q[h][s] : __dadd_rn(uc, __dmul_rn(p.omega, q[h][s]));
         U[A + 2 * h][RC][s] = (!EDGE || ok[h][s]) ? out : uc;
@@ -362,16 +445,10 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     }
     if (pzin) {
 #pragma unroll
-      for (int h = 0; h < H; ++h)
-        *reinterpret_cast<double2 *>(pc + (A + 2 * h) * G::PX) =
-            make_double2(U[A + 2 * h][RC][0], U[A + 2 * h][RC][1]);
+      for (int h = 0; h < H; ++h) st_row(pcs + (A + 2 * h) * G::PX, U[A + 2 * h][RC]);
     } else {
 #pragma unroll
-      for (int h = 0; h < H; ++h) {
-        const double2 v = *reinterpret_cast<const double2 *>(pc + (A + 2 * h) * G::PX);
-        U[A + 2 * h][RC][0] = v.x;
-        U[A + 2 * h][RC][1] = v.y;
-      }
+      for (int h = 0; h < H; ++h) ld_row(pcs + (A + 2 * h) * G::PX, U[A + 2 * h][RC]);
     }
   };
 
@@ -385,68 +462,67 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
       const bool zin = po >= 1 && po <= nz;
 #pragma unroll
       for (int a = 0; a < RT; ++a)
-        if ((ownbits >> a) & 1u) {
-          stg_pair(dp + a * sy32, U[a][E][0], U[a][E][1]);
-          stg_pair_peers<PEER>(p, po, (int64_t)po * sz + rowoff0 + a * sy32, U[a][E][0], U[a][E][1]);
-          if (zin) {
 #pragma unroll
-            for (int s = 0; s < 2; ++s) {
-              const unsigned ex = (unsigned)__double2hiint(U[a][E][s]) & 0x7ff00000u;
-              emax = max(emax, (!EDGE || ((inbits >> (2 * a + s)) & 1u)) ? ex : 0u);
+        for (int pr = 0; pr < CP; ++pr)
+          if ((ownbits >> (a * CP + pr)) & 1u) {
+            stg_pair(dp + a * sy32 + 2 * pr, U[a][E][2 * pr], U[a][E][2 * pr + 1]);
+            stg_pair_peers<PEER>(p, po, (int64_t)po * sz + rowoff0 + a * sy32 + 2 * pr, U[a][E][2 * pr],
+                                 U[a][E][2 * pr + 1]);
+            if (zin) {
+#pragma unroll
+              for (int s = 2 * pr; s < 2 * pr + 2; ++s) {
+                const unsigned ex = (unsigned)__double2hiint(U[a][E][s]) & 0x7ff00000u;
+                emax = max(emax, (!EDGE || ((inbits >> (C * a + s)) & 1u)) ? ex : 0u);
+              }
             }
           }
-        }
     }
   };
 
-  for (int pp0 = p_begin; pp0 <= p_end; pp0 += 4) {
-    [&]<int... Ks>(std::integer_sequence<int, Ks...>) {
-      (
-          [&] {
-            constexpr int KS = Ks;                      // pair step within the ring turn
-            constexpr int RP0 = (2 + 2 * KS) % RR;      // ring entry of the pair plane pp
-            constexpr int RM1 = (RP0 + RR - 1) % RR;
-            const int pp = pp0 + 2 * KS;
-            // planes pp-1 and pp -> ring (plane pp+1 is read from its slot:
-            // only three planes are ever live in registers)
-            wait_plane(pp);
-            wait_plane(pp + 1);
-            {
-              const double *pa = slot_of(pp - 1), *pb = slot_of(pp);
+  // one pair step per iteration (not unrolled: with four columns per lane a
+  // second unrolled step made the loop outgrow the instruction cache —
+  // no_instructions was the top stall — and the ring turn it saved is 2 % of
+  // the step's instructions)
+  constexpr int RP0 = 2, RM1 = 1;
+#pragma unroll 1
+  for (int pp = p_begin; pp <= p_end; pp += 2) {
+    // planes pp-1 and pp -> ring
+    wait_plane(pp);
+    wait_plane(pp + 1);
+    {
+      const double *pa = slot_of(pp - 1), *pb = slot_of(pp);
 #pragma unroll
-              for (int a = 0; a < RT; ++a) {
-                const double2 va = *reinterpret_cast<const double2 *>(pa + a * G::PX);
-                const double2 vb = *reinterpret_cast<const double2 *>(pb + a * G::PX);
-                U[a][RM1][0] = va.x;
-                U[a][RM1][1] = va.y;
-                U[a][RP0][0] = vb.x;
-                U[a][RP0][1] = vb.y;
-              }
-            }
-            group.template operator()<0, RP0>(pp);
-            __syncthreads();
-            // everybody is past the previous pair step: refill the slots of
-            // planes pp-4, pp-3 with planes pp+4, pp+5
-            if (threadIdx.x == 0) {
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              issue(pp + 4);
-              issue(pp + 5);
-            }
-            group.template operator()<1, RP0>(pp);
-            store_plane(pp, std::integral_constant<int, RP0>{});  // plane pp is final after G1
-            __syncthreads();
-            group.template operator()<2, RP0>(pp);
-            __syncthreads();
-            group.template operator()<3, RP0>(pp);
-            store_plane(pp - 1, std::integral_constant<int, RM1>{});
-          }(),
-          ...);
-    }(std::make_integer_sequence<int, 2>{});
+      for (int a = 0; a < RT; ++a) {
+        ld_row(pa + a * G::PX, U[a][RM1]);
+        ld_row(pb + a * G::PX, U[a][RP0]);
+      }
+    }
+    group.template operator()<0, RP0>(pp);
+    __syncthreads();
+    // everybody is past the previous pair step: refill the slots of
+    // planes pp-4, pp-3 with planes pp+S-4, pp+S-3
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(pp + G::S - 4);
+      issue(pp + G::S - 3);
+    }
+    group.template operator()<1, RP0>(pp);
+    store_plane(pp, std::integral_constant<int, RP0>{});  // plane pp is final after G1
+    __syncthreads();
+    group.template operator()<2, RP0>(pp);
+    __syncthreads();
+    group.template operator()<3, RP0>(pp);
+    store_plane(pp - 1, std::integral_constant<int, RM1>{});
+    // plane pp is the next step's plane pp-2
+#pragma unroll
+    for (int a = 0; a < RT; ++a)
+#pragma unroll
+      for (int c = 0; c < C; ++c) U[a][0][c] = U[a][RP0][c];
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // drain the copies issued but never waited for
-    const int pl_end = p_begin + ((p_end - p_begin) / 4 + 1) * 4;  // first pair step not run
-    for (int pl = pl_end; pl <= pl_end + 3; ++pl) wait_plane(pl);
+    const int pl_end = p_begin + ((p_end - p_begin) / 2 + 1) * 2;  // first pair step not run
+    for (int pl = pl_end; pl <= pl_end + G::S - 5; ++pl) wait_plane(pl);
   }
   __syncthreads();
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -465,8 +541,9 @@ k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__
   const int tx = item % (int)ntx, ty = (item / (int)ntx) % (int)nty;
   const int x0 = (int)(2 * (((int64_t)tx * (Sx / 2)) / ntx));
   const int y0 = (int)(((int64_t)ty * Sy) / nty);
-  const bool edge = x0 - G::GX < 1 || x0 - G::GX + G::PX > (int)p.nx + 1 || y0 - G::GY < 1 ||
-                    y0 - G::GY + G::BOXY > (int)p.ny + 1;
+  const int gy0 = G::SHIFT ? y0 - G::GY - ((1 - p.py - (y0 - G::GY)) & 1) : y0 - G::GY;
+  const bool edge = x0 - G::GX < 1 || x0 - G::GX + G::PX > (int)p.nx + 1 || gy0 < 1 ||
+                    gy0 + G::BOXY > (int)p.ny + 1;
   if (edge)
     q1col_body<FORM, UNIT, DIV, PEER, true>(p, tmu, dst, ntx, nty, nzc);
   else

@@ -44,7 +44,10 @@ for r in rows[2:]:
         continue
     op = r[sc].strip().split()
     o = op[1] if op[0].startswith("@") else op[0]
-    n = int(r[ie] or 0)
+    try:
+        n = int(r[ie] or 0)
+    except ValueError:
+        continue
     cnt[o.split(".")[0]] += n
     tot += n
 scale = 32 / pts if pts else 1 / tot * 100

@@ -4,7 +4,8 @@ so a race that changed a value would show as a mismatch too.
 
     compute-sanitizer --tool racecheck python tools/race_run.py [case ...]
 
-Cases: strip2d (FE9, k2_strip2d), fd5strip (FD5 2 sweeps/pass), block2d (K4),
+Cases: strip2d (FE9, k2_strip2d), fd5strip (FD5 2 sweeps/pass), block2d (K4, FE9),
+resident (K6, FD5 on chip across sweeps),
 col3d (FD7, k2_col3d_fd7), q1col (FE27-Q1, k2_q1col), stream3d (FE27 reference
 weights), patch (K3), k1 (per-colour), lex (hyperplanes), peer (slab pass with
 fused peer stores, emulated on one device).
@@ -68,7 +69,8 @@ def peer_case():
 CASES = {
     "strip2d": lambda: grid_case("fe9", 300, 2, _native.SL_FLAG_STREAM),   # streaming kernel forced
     "fd5strip": lambda: grid_case("fd5", 300, 2, _native.SL_FLAG_STREAM),
-    "block2d": lambda: grid_case("fd5", 200, 5) and grid_case("fe9", 150, 3),
+    "block2d": lambda: grid_case("fe9", 150, 3) and grid_case("fe9", 201, 2),
+    "resident": lambda: grid_case("fd5", 200, 5) and grid_case("fd5", 1024, 3),   # K6, on-chip across sweeps
     "col3d": lambda: grid_case("fd7", 70, 2),
     "q1col": lambda: grid_case("fe27q1", 70, 2),
     "stream3d": lambda: grid_case("fe27", 40, 2),

@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 CS=/usr/local/cuda/bin/compute-sanitizer
-for c in strip2d fd5strip block2d col3d q1col stream3d patch k1 lex peer; do
+for c in ${CASES:-strip2d fd5strip block2d resident col3d q1col stream3d patch k1 lex peer}; do
   for tool in racecheck synccheck memcheck; do
     extra=""
     [ $tool = racecheck ] && extra="--racecheck-report all"
