@@ -15,6 +15,47 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// -DSL_FUZZ: timing-perturbation build (tools/fuzz_race.sh).  compute-sanitizer
+// is closed on the GPU pool, so the evidence that the smem rings, mbarriers and
+// inter-CTA flags order every access is statistical: sl_fuzz() delays the
+// calling warp by a pseudo-random 0..4095 cycles (a quarter of the visits) on
+// both sides of every block/warp barrier, after every mbarrier wait, before
+// every TMA issue and around the K6 flag accesses; the bitwise parity suite
+// must stay green under it.  -DSL_FUZZ_BREAK=n removes one needed barrier
+// (negative controls: the suite must then fail).
+#ifdef SL_FUZZ
+// lanes = true: the delay also depends on the lane (sites followed by a warp barrier)
+__device__ __forceinline__ void sl_fuzz(unsigned site, bool lanes = false) {
+  unsigned h = (unsigned)clock64() * 2654435761u;
+  h ^= blockIdx.x * 40503u + (lanes ? threadIdx.x : (threadIdx.x >> 5)) * 9176u + site * 0x9e3779b9u;
+  h ^= h >> 15;
+  h *= 0x2c1b3c6du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) {
+    const long long d = (h >> 8) & 4095u, t0 = clock64();
+    while (clock64() - t0 < d) {
+    }
+  }
+}
+#define __syncthreads()             \
+  do {                              \
+    sl_fuzz(__LINE__);              \
+    ::__syncthreads();              \
+    sl_fuzz(__LINE__ + 50000u);     \
+  } while (0)
+#define __syncwarp()                \
+  do {                              \
+    sl_fuzz(__LINE__ + 100000u, true); \
+    ::__syncwarp();                 \
+    sl_fuzz(__LINE__ + 150000u);    \
+  } while (0)
+#else
+#define sl_fuzz(...) ((void)0)
+#endif
+#ifndef SL_FUZZ_BREAK
+#define SL_FUZZ_BREAK 0
+#endif
+
 namespace sl {
 
 // bench evidence: kernels launched by this library (capi.cu)

@@ -69,6 +69,7 @@ __device__ __forceinline__ void mbar_init3(uint32_t addr) {
 }
 
 __device__ __forceinline__ void mbar_expect3(uint32_t addr, uint32_t bytes) {
+  sl_fuzz(220000u);   // before a slot is re-armed and refilled
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(addr), "r"(bytes) : "memory");
 }
 
@@ -79,6 +80,7 @@ __device__ __forceinline__ void mbar_wait3(uint32_t addr, uint32_t parity) {
       "@!P1 bra W3_%=;\n}\n" ::"r"(addr),
       "r"(parity)
       : "memory");
+  sl_fuzz(210000u);
 }
 
 template <int FORM, bool UNIT, int DIV, bool PEER = false>
@@ -276,7 +278,9 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
                   stg_pair_peers<PEER>(p, pz, e, U[a][SM2][0], U[a][SM2][1]);
                 }
             }
+#if SL_FUZZ_BREAK != 3
             __syncthreads();
+#endif
             // slots of planes t-3 (u) / t-4 (f) are free: refill them D planes ahead
             if (threadIdx.x == 0) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

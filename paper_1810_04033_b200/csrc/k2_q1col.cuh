@@ -508,7 +508,9 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     }
     group.template operator()<1, RP0>(pp);
     store_plane(pp, std::integral_constant<int, RP0>{});  // plane pp is final after G1
+#if SL_FUZZ_BREAK != 1
     __syncthreads();
+#endif
     group.template operator()<2, RP0>(pp);
     __syncthreads();
     group.template operator()<3, RP0>(pp);

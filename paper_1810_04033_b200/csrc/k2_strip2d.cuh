@@ -89,6 +89,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
       "}\n" ::"r"(addr),
       "r"(parity)
       : "memory");
+  sl_fuzz(200000u);
 }
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
@@ -211,7 +212,9 @@ k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, i
             {
               constexpr int SL = KS % NS;
               constexpr int RR = (KS + 1) % NRR;
+#if SL_FUZZ_BREAK != 2   // negative control: read the row slot without waiting for its TMA copy
               mbar_wait(mb0 + 8u * SL, (round + (uint32_t)(KS / NS)) & 1u);
+#endif
               const uint32_t a = ring + SL * G::SLOTB + lane * (NC * 8u);
 #pragma unroll
               for (int k = 0; k < NP; ++k) {

@@ -52,10 +52,12 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  sl_fuzz(230000u);
   return v;
 }
 
 __device__ __forceinline__ void st_release_gpu(int *p, int v) {
+  sl_fuzz(240000u);
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 

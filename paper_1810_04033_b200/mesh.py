@@ -75,11 +75,26 @@ class Mesh:
 
     @property
     def values(self) -> np.ndarray:
-        """Host view of the buffer (synchronises with the device first)."""
+        """Writable host view of the buffer (synchronises with the device
+        first).  The caller may mutate it, so the host copy becomes the
+        authoritative one and the next device call uploads it again; readers
+        that only look use `read_values()`, which skips that upload."""
         if self._where == "dev":
             self._dev_to_host()
         self._where = "host"   # the caller may mutate it
         return self._host
+
+    def read_values(self) -> np.ndarray:
+        """Read-only host view of the buffer.  Unlike `values` it leaves the
+        device copy authoritative, so the next sweep does not upload the
+        whole grid again (8.6 GB for BASELINE config 4): use it for digests,
+        comparisons and output.  The view is valid until the next device
+        call; writes go through `values`."""
+        if self._where == "dev":
+            self._dev_to_host()
+        view = self._host.view()
+        view.flags.writeable = False
+        return view
 
     @values.setter
     def values(self, arr):

@@ -184,3 +184,25 @@ def test_stencil_lab_import_name_reaches_the_gpu_package():
     assert Schedule is sl.Schedule
     with pytest.raises(ImportError, match="nested dissection"):
         from stencil_lab import dissect  # noqa: F401
+
+
+def test_read_values_is_read_only_and_keeps_the_device_authoritative():
+    """`values` hands out a writable view (reference semantics) and therefore
+    marks the host copy authoritative; `read_values` must not."""
+    class HostOnly(type(sl.make_mesh(2, 6, seed=5))):
+        __slots__ = ()
+
+        def _dev_to_host(self):           # no GPU here: the "download" is a no-op
+            pass
+
+    m = HostOnly(2, 6)
+    sl.init(m, 5)
+    m._where = "dev"                      # as after a device sweep
+    v = m.read_values()
+    assert m._where == "dev"
+    assert not v.flags.writeable
+    with pytest.raises(ValueError):
+        v[0] = 1.0
+    assert np.array_equal(v, m._host)
+    m.values[0] = 2.0                     # the writable accessor flips the state
+    assert m._where == "host" and m._host[0] == 2.0

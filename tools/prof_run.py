@@ -21,10 +21,15 @@ ap.add_argument("--per-colour", action="store_true")
 a = ap.parse_args()
 wl = CONFIGS[a.config]
 kind = sl.get_stencil(wl.stencil)
-m = sl.Mesh(wl.dim, wl.n)
-sl.init(m, wl.seed)
-sl.init_rhs(m, wl.seed + 1, wl.omega)
 flags = _native.SL_FLAG_PER_COLOUR if a.per_colour else 0
-sl.run_sweeps(m, kind, sl.CostModel(), a.sweeps, flags=flags)
+if wl.batch > 1:
+    u0, f0 = sl.init_patches(wl.batch, wl.n, wl.seed)
+    pb = sl.PatchBatch(torch.from_numpy(u0), torch.from_numpy(f0), wl.omega)
+    pb.sweep(kind, a.sweeps, flags=flags)
+else:
+    m = sl.Mesh(wl.dim, wl.n)
+    sl.init(m, wl.seed)
+    sl.init_rhs(m, wl.seed + 1, wl.omega)
+    sl.run_sweeps(m, kind, sl.CostModel(), a.sweeps, flags=flags)
 torch.cuda.synchronize()
 print("ok", wl.name, a.sweeps)
