@@ -28,7 +28,11 @@ namespace sl {
 
 template <int S, int M>
 struct GeoS2 {
-  static constexpr FPlan P = make_plan(S, S == FE9 ? 4 : 2, M);
+#ifndef STRIP_SPREAD
+#define STRIP_SPREAD 0
+#endif
+  // STRIP_SPREAD = 1 (A/B): spread lags, so the phases active in one step are independent
+  static constexpr FPlan P = make_plan(S, S == FE9 ? 4 : 2, M, STRIP_SPREAD != 0 && S == FE9 && M == 1);
   static constexpr int K = P.K, C = P.C, LAGMAX = P.lagmax;
   static constexpr bool RB = (P.C == 2);
   static constexpr int GX = (P.load[0] + 1) & ~1;
