@@ -111,7 +111,11 @@ static __device__ __noinline__ double strip_div_exact(double a, double b) { retu
 // points and, through the shuffle, by the adjacent lane — the same rounded
 // terms, added in the same canonical order.
 template <int S, int FORM, bool UNIT, int DIV, int M, bool EQW = false, bool PEER = false>
-__global__ void __launch_bounds__(32 * GeoS2<S, M>::WPB)
+#ifndef STRIP_MINB
+#define STRIP_MINB 1
+#endif
+// STRIP_MINB (A/B): minimum resident blocks per SM asked of ptxas (caps the registers)
+__global__ void __launch_bounds__(32 * GeoS2<S, M>::WPB, STRIP_MINB)
 k2_strip2d(Params p, const double *__restrict__ src, double *__restrict__ dst, int64_t nstrip,
            int64_t nchunk) {
   using G = GeoS2<S, M>;
