@@ -279,6 +279,26 @@ def test_host_edits_between_sweeps_are_seen():
     assert (m.values == 2.0).all()
 
 
+def test_read_values_between_sweeps_keeps_the_device_authoritative():
+    """read_values() downloads without flipping the mesh to host-authoritative
+    (no re-upload on the next sweep), is read-only, and the sweeps continue
+    from the device state: 2 + 3 sweeps with a read in between == 5 sweeps."""
+    n, seed = 70, 12
+    m = sl.make_mesh(2, n, seed=seed)
+    sl.init_rhs(m, seed + 1, 0.8)
+    sl.run_sweeps(m, sl.FE9, sl.CostModel(), 2)
+    mid = m.read_values()
+    assert m._where == "dev" and not mid.flags.writeable
+    want = R.init_u(2, n, seed)
+    f = R.init_f(2, n, seed + 1)
+    coracle.sweep(want, "fe9", 2, f=f, omega=0.8, form="D")
+    assert _bits_equal(mid, want)
+    m._host.fill(-7.0)                 # a stale host mirror must not come back
+    sl.run_sweeps(m, sl.FE9, sl.CostModel(), 3)
+    coracle.sweep(want, "fe9", 3, f=f, omega=0.8, form="D")
+    assert _bits_equal(m.read_values(), want)
+
+
 # -- lexicographic order (serial / taskgraph) ---------------------------------
 
 @pytest.mark.parametrize("strategy", ["serial", "taskgraph"])
