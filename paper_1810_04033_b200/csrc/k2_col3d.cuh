@@ -225,6 +225,9 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
           [&] {
             constexpr int KS = Ks;
             const int t = t0 + KS;
+            // the unrolled round is left at the chunk's last step (CTA-uniform): a thin
+            // slab's chunk is ~28 steps, so rounding up to R = 6 would cost it up to 18 %
+            if (t > t_end) return;
             constexpr int S1 = (KS + 1) % R, S0 = KS % R, SM1 = (KS + R - 1) % R;
             constexpr int SM2 = (KS + R - 2) % R, SM3 = (KS + R - 3) % R;
             // ---- plane t+1: smem slot -> register ring (use count of slot S1) ----
@@ -293,7 +296,7 @@ k2_col3d_fd7(Params p, const __grid_constant__ CUtensorMap tmu, const __grid_con
   }
   // drain the copies still in flight before the CTA exits
   if (threadIdx.x == 0) {
-    const int tl = t_begin + (int)round * R;  // first unprocessed step
+    const int tl = t_end + 1;  // first unprocessed step
     for (int k = 0; k <= D; ++k) {
       const int pu = tl + 1 + k, pf = tl + k;
       const int su_i = (pu - t_begin) % R, sf_i = (pf - t_begin) % R;

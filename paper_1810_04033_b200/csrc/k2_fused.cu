@@ -540,7 +540,8 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     if (e != cudaSuccess) return e;
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
     const int64_t ntx = (Sx + G::TX - 1) / G::TX, nty = (Sy + G::TY - 1) / G::TY;
-    const int64_t nzc = pick_chunks(ntx * nty, p.zhi - p.zlo, slots, G::GZ + G::LAGMAX + G::R, 16);
+    // per chunk: GZ + 1 (+1 parity) ghost planes, LAGMAX drain steps and the ring fill
+    const int64_t nzc = pick_chunks(ntx * nty, p.zhi - p.zlo, slots, G::GZ + G::LAGMAX + 4, 16);
     kern<<<(unsigned)(ntx * nty * nzc), G::NT, G::SMEM, st>>>(p, tmu, tmf, dst, ntx, nty, nzc);
     note_launch();
     return cudaGetLastError();
