@@ -560,6 +560,27 @@ static cudaError_t launch_pass(const Params &p, const double *src, double *dst, 
     if (e != cudaSuccess) return e;
     const int64_t Sx = p.nx + 2, Sy = p.ny + 2, Sz = p.nz + 2;
     const int64_t ntx = (Sx + G::TX - 1) / G::TX, nty = (Sy + G::TY - 1) / G::TY;
+    if constexpr (G::CL) {
+      // nty counts pairs of tiles: each is one thread-block cluster of two CTAs along y
+      const int64_t nzc = pick_chunks(2 * ntx * nty, p.zhi - p.zlo, slots, G::GZ + G::LAGMAX + G::RR, 16);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(2 * ntx * nty * nzc));
+      cfg.blockDim = dim3(G::NT);
+      cfg.dynamicSmemBytes = G::SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      double *dstp = dst;
+      int64_t a_ntx = ntx, a_nty = nty, a_nzc = nzc;
+      cudaError_t el = cudaLaunchKernelEx(&cfg, kern, p, tmu, dstp, a_ntx, a_nty, a_nzc);
+      note_launch();
+      return el != cudaSuccess ? el : cudaGetLastError();
+    }
     const int64_t nzc = pick_chunks(ntx * nty, p.zhi - p.zlo, slots, G::GZ + G::LAGMAX + G::RR, 16);
     kern<<<(unsigned)(ntx * nty * nzc), G::NT, G::SMEM, st>>>(p, tmu, dst, ntx, nty, nzc);
     note_launch();

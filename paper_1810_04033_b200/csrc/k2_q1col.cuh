@@ -76,15 +76,26 @@ static __device__ __noinline__ double q1_div_exact(double a, double b) { return 
 #ifndef Q1_SHIFT
 #define Q1_SHIFT 0
 #endif
+// Q1_CLUSTER = 1 (A/B): CTAs run as thread-block clusters of two along y.  The
+// pair shares its facing edge: neither CTA carries ghost rows there; each
+// reads the other's boundary row from one extra row of its own plane slots,
+// which the owner refreshes with st.shared::cluster after every group that
+// updates it, and the three block barriers of a pair step become cluster
+// barriers.  A pair owns up to 2 (PY - GY) - 2 rows for 2 PY computed rows.
+#ifndef Q1_CLUSTER
+#define Q1_CLUSTER 0
+#endif
 struct Q1Geo {
   static constexpr FPlan P = make_plan(Q1, 8, 1, false);
+  static constexpr bool CL = Q1_CLUSTER != 0;
   static constexpr int GX = 4, GY = 4, GZ = 2;            // plan load margins
   static constexpr int CPL = Q1_CPL;                      // columns per lane
   static constexpr int LX = Q1_LX, LY = 32 / LX;          // lanes along x / lane rows per warp
   static constexpr int PX = CPL * LX, PY = Q1_PY;         // tile incl. ghost
   static constexpr bool SHIFT = Q1_SHIFT != 0;
   static constexpr int BOXY = SHIFT ? PY : PY + 1;        // rows loaded
-  static constexpr int TX = PX - 2 * GX, TY = PY - 2 * GY - (SHIFT ? 1 : 0);
+  // rows owned per tile (per pair of tiles with CL)
+  static constexpr int TX = PX - 2 * GX, TY = CL ? 2 * (PY - GY) - 2 : PY - 2 * GY - (SHIFT ? 1 : 0);
   static constexpr int S = Q1_S;                          // smem slots (4 live planes + S - 4 ahead)
   static constexpr int RR = 4;                            // ring entries (planes p-2 .. p live)
   static constexpr int RT = Q1_RT;                        // tile rows per thread
@@ -98,7 +109,18 @@ struct Q1Geo {
   static_assert(CPL % 2 == 0 && LX * LY == 32 && PY % (RT * LY) == 0 && S >= 6 && (S & 1) == 0, "geometry");
   static_assert(4 * (RT / 2) * CPL <= 32 && RT * CPL <= 32, "mask bits");
   static_assert(SMEM <= 227 * 1024, "shared memory");
+  static_assert(!CL || (CPL == 2 && !SHIFT && LX == 32), "cluster pairs: column-pair geometry only");
 };
+
+__device__ __forceinline__ void q1_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// store a value pair at the same shared-memory offset in CTA `peer` of the cluster
+__device__ __forceinline__ void q1_push_pair(const double *own, unsigned peer, double a, double b) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"((uint32_t)__cvta_generic_to_shared(own)), "r"(peer));
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(ra), "d"(a), "d"(b) : "memory");
+}
 
 constexpr bool q1_plan_ok() {
   for (int k = 0; k < 8; ++k)
@@ -129,10 +151,20 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
 
   const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2, Sz = (int)p.nz + 2;
   const int nx = (int)p.nx, ny = (int)p.ny, nz = (int)p.nz;
-  const int item = blockIdx.x;
+  const int item = G::CL ? blockIdx.x >> 1 : blockIdx.x;
+  const int crank = G::CL ? (int)(blockIdx.x & 1) : 0;   // rank in the cluster pair (CL)
   const int tx = item % (int)ntx, ty = (item / (int)ntx) % (int)nty, zc = item / (int)(ntx * nty);
   const int x0 = (int)(2 * (((int64_t)tx * (Sx / 2)) / ntx)), x1 = (int)(2 * (((int64_t)(tx + 1) * (Sx / 2)) / ntx));
-  const int y0 = (int)(((int64_t)ty * Sy) / nty), y1 = (int)(((int64_t)(ty + 1) * Sy) / nty);
+  int y0 = (int)(((int64_t)ty * Sy) / nty), y1 = (int)(((int64_t)(ty + 1) * Sy) / nty);
+  // CL: [y0, y1) is the pair's range; it is split at ymid, a row of y parity 0,
+  // rank 0 computes the PY rows below ymid (global ymid - PY .. ymid - 1), rank 1
+  // the PY rows from ymid on
+  int ymid = 0;
+  if (G::CL) {
+    ymid = (y0 + y1) / 2;
+    if ((ymid - 1 + p.py) & 1) ++ymid;
+    if (crank == 0) y1 = ymid; else y0 = ymid;
+  }
   const int zlen = p.zhi - p.zlo;
   const int z0 = p.zlo + (int)(((int64_t)zc * zlen) / nzc), z1 = p.zlo + (int)(((int64_t)(zc + 1) * zlen) / nzc);
   const int TXo = x1 - x0, TYo = y1 - y0;
@@ -142,10 +174,15 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
   const int vrow = warp * G::LY + lane / G::LX;  // band of RT rows
   const int gx = gx0 + C * lx;
   // local row r0 has y parity 0; the tile's first owned row is local row TM
-  const int delta = (1 - p.py - (y0 - G::GY)) & 1;
-  const int gy0 = G::SHIFT ? y0 - G::GY - delta : y0 - G::GY;
-  const int TM = G::SHIFT ? G::GY + delta : G::GY;
+  // CL: rank 0's local rows 0 .. PY-1 end at the shared edge and local row PY
+  // is rank 1's first row; rank 1's local row 0 is rank 0's last row and its
+  // own rows are 1 .. PY
+  const int delta = G::CL ? crank : (1 - p.py - (y0 - G::GY)) & 1;
+  const int gy0 = G::CL ? (crank == 0 ? ymid - G::PY : ymid - 1) : G::SHIFT ? y0 - G::GY - delta : y0 - G::GY;
+  const int TM = G::CL ? y0 - gy0 : G::SHIFT ? G::GY + delta : G::GY;
   const int r0 = G::SHIFT ? RT * vrow : RT * vrow + delta;   // this thread's rows r0 (qy 0) .. r0 + RT - 1
+  // no ghost rows (and no decay of the need region) on the side shared with the cluster peer
+  const bool sh_lo = G::CL && crank == 1, sh_hi = G::CL && crank == 0;
   const int64_t sz = p.sz;
 
   // pair steps at planes pp = p_begin, p_begin + 2, ... of parity qz = 0;
@@ -227,7 +264,7 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
 #pragma unroll
     for (int h = 0; h < H; ++h) {
       const int r = r0 + A + 2 * h, gy = gy0 + r;
-      const bool rok = r >= TM - nyj && r < TM + TYo + nyj && gy >= 1 && gy <= ny;
+      const bool rok = r >= TM - (sh_lo ? 0 : nyj) && r < TM + TYo + (sh_hi ? 0 : nyj) && gy >= 1 && gy <= ny;
 #pragma unroll
       for (int s = 0; s < C; ++s) {
         const int lc = C * lx + s;
@@ -446,6 +483,17 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     if (pzin) {
 #pragma unroll
       for (int h = 0; h < H; ++h) st_row(pcs + (A + 2 * h) * G::PX, U[A + 2 * h][RC]);
+      if constexpr (G::CL) {
+        // the row facing the cluster peer also goes into the peer's copy of it:
+        // rank 0's last row (local PY - 1, updated by the A = 1 groups) is the
+        // peer's local row 0; rank 1's first row (local 1, A = 0 groups) is the
+        // peer's local row PY
+        constexpr int AR = A == 1 ? RT - 1 : 0;   // this group's candidate row of the thread
+        if (A == 1 && crank == 0 && vrow == G::PY / RT - 1)
+          q1_push_pair(pcs + (AR - (G::PY - 1)) * G::PX, 1u, U[AR][RC][0], U[AR][RC][1]);
+        if (A == 0 && crank == 1 && vrow == 0)
+          q1_push_pair(pcs + (G::PY - 1) * G::PX, 0u, U[AR][RC][0], U[AR][RC][1]);
+      }
     } else {
 #pragma unroll
       for (int h = 0; h < H; ++h) ld_row(pcs + (A + 2 * h) * G::PX, U[A + 2 * h][RC]);
@@ -479,11 +527,27 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     }
   };
 
+  // between colour groups: the block's warps — and with CL the cluster peer, whose
+  // boundary row each group may read — must have published the previous group
+  auto group_sync = [&] {
+    if constexpr (G::CL) {
+      sl_fuzz(300000u);
+      q1_cluster_sync();
+      sl_fuzz(310000u);
+    } else {
+      __syncthreads();
+    }
+  };
   // one pair step per iteration (not unrolled: with four columns per lane a
   // second unrolled step made the loop outgrow the instruction cache —
   // no_instructions was the top stall — and the ring turn it saved is 2 % of
   // the step's instructions)
   constexpr int RP0 = 2, RM1 = 1;
+  if constexpr (G::CL) {   // both CTAs run, and their first planes have landed, before any peer store
+    wait_plane(p_begin);
+    wait_plane(p_begin + 1);
+    q1_cluster_sync();
+  }
 #pragma unroll 1
   for (int pp = p_begin; pp <= p_end; pp += 2) {
     // planes pp-1 and pp -> ring
@@ -498,7 +562,7 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
       }
     }
     group.template operator()<0, RP0>(pp);
-    __syncthreads();
+    group_sync();
     // everybody is past the previous pair step: refill the slots of
     // planes pp-4, pp-3 with planes pp+S-4, pp+S-3
     if (threadIdx.x == 0) {
@@ -509,10 +573,18 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     group.template operator()<1, RP0>(pp);
     store_plane(pp, std::integral_constant<int, RP0>{});  // plane pp is final after G1
 #if SL_FUZZ_BREAK != 1
-    __syncthreads();
+    group_sync();
 #endif
     group.template operator()<2, RP0>(pp);
-    __syncthreads();
+    // CL: the peer stores its boundary row of plane pp+2 into this CTA's slot
+    // when its next G0 ends; this CTA's own TMA copy of that plane (which
+    // covers the same row) must have landed before, i.e. before the last
+    // barrier the peer passes on its way there
+    if constexpr (G::CL) {
+      wait_plane(pp + 2);
+      wait_plane(pp + 3);
+    }
+    group_sync();
     group.template operator()<3, RP0>(pp);
     store_plane(pp - 1, std::integral_constant<int, RM1>{});
     // plane pp is the next step's plane pp-2
@@ -527,6 +599,7 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     for (int pl = pl_end; pl <= pl_end + G::S - 5; ++pl) wait_plane(pl);
   }
   __syncthreads();
+  if constexpr (G::CL) q1_cluster_sync();   // the peer may still be storing into this CTA's slots
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (__any_sync(0xffffffffu, emax == 0x7ff00000u) && lane == 0) atomicOr(p.status, 1);
 }
@@ -536,14 +609,20 @@ __global__ void __launch_bounds__(Q1Geo::NT, 1)
 k2_q1col(Params p, const __grid_constant__ CUtensorMap tmu, double *__restrict__ dst, int64_t ntx,
          int64_t nty, int64_t nzc) {
   using G = Q1Geo;
-  // interior tile: its loaded window [x0 - GX, x0 - GX + PX) x [y0 - GY, y0 - GY + BOXY)
+  // interior tile: its loaded window [x0 - GX, x0 - GX + PX) x [gy0, gy0 + BOXY)
   // lies in [1, n] in x and y (same tile arithmetic as the body)
   const int Sx = (int)p.nx + 2, Sy = (int)p.ny + 2;
-  const int item = blockIdx.x;
+  const int item = G::CL ? blockIdx.x >> 1 : blockIdx.x;
   const int tx = item % (int)ntx, ty = (item / (int)ntx) % (int)nty;
   const int x0 = (int)(2 * (((int64_t)tx * (Sx / 2)) / ntx));
   const int y0 = (int)(((int64_t)ty * Sy) / nty);
-  const int gy0 = G::SHIFT ? y0 - G::GY - ((1 - p.py - (y0 - G::GY)) & 1) : y0 - G::GY;
+  int gy0 = G::SHIFT ? y0 - G::GY - ((1 - p.py - (y0 - G::GY)) & 1) : y0 - G::GY;
+  if (G::CL) {
+    const int y1 = (int)(((int64_t)(ty + 1) * Sy) / nty);
+    int ymid = (y0 + y1) / 2;
+    if ((ymid - 1 + p.py) & 1) ++ymid;
+    gy0 = (blockIdx.x & 1) == 0 ? ymid - G::PY : ymid - 1;
+  }
   const bool edge = x0 - G::GX < 1 || x0 - G::GX + G::PX > (int)p.nx + 1 || gy0 < 1 ||
                     gy0 + G::BOXY > (int)p.ny + 1;
   if (edge)
