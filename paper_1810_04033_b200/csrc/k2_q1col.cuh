@@ -571,10 +571,13 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
       issue(pp + G::S - 3);
     }
     group.template operator()<1, RP0>(pp);
-    store_plane(pp, std::integral_constant<int, RP0>{});  // plane pp is final after G1
+    // plane pp is final after G1.  With CL its global stores are issued after the barrier: a
+    // cluster arrive.release right behind them would wait for their acknowledgement
+    if constexpr (!G::CL) store_plane(pp, std::integral_constant<int, RP0>{});
 #if SL_FUZZ_BREAK != 1
     group_sync();
 #endif
+    if constexpr (G::CL) store_plane(pp, std::integral_constant<int, RP0>{});
     group.template operator()<2, RP0>(pp);
     // CL: the peer stores its boundary row of plane pp+2 into this CTA's slot
     // when its next G0 ends; this CTA's own TMA copy of that plane (which
