@@ -465,6 +465,10 @@ static cudaError_t make_tmap3(CUtensorMap *map, const double *base, const Params
   return cudaSuccess;
 }
 
+// L2 promotion of the plane loads (A/B: -DSL_TMAP_PROMO=CU_TENSOR_MAP_L2_PROMOTION_L2_128B / _NONE)
+#ifndef SL_TMAP_PROMO
+#define SL_TMAP_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 static cudaError_t encode_tmap3(CUtensorMap *map, const double *base, const Params &p, int boxx,
                                 int boxy) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -481,7 +485,7 @@ static cudaError_t encode_tmap3(CUtensorMap *map, const double *base, const Para
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides,
                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      SL_TMAP_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
