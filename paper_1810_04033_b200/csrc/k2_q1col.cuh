@@ -104,7 +104,7 @@ struct Q1Geo {
   static constexpr int SLOTE = PX * BOXY;
   static constexpr int LEADE = 2 * PX;                    // guard rows before slot 0
   static constexpr int FBUFE = 2 * (RT / 2) * CPL * NT;   // f staging: 2 buffers x H rows x PX cols per lane row
-  static constexpr size_t SMEM = size_t(LEADE + S * SLOTE + 2 * PX + FBUFE) * sizeof(double) + S * 8;
+  static constexpr size_t SMEM = size_t(LEADE + S * SLOTE + 2 * PX + FBUFE) * sizeof(double) + S * 8 + (CL ? 4 * 8 : 0);
   static_assert(P.load[0] <= GX && P.load[1] <= GY && P.load[2] <= GZ, "ghost margin");
   static_assert(CPL % 2 == 0 && LX * LY == 32 && PY % (RT * LY) == 0 && S >= 6 && (S & 1) == 0, "geometry");
   static_assert(4 * (RT / 2) * CPL <= 32 && RT * CPL <= 32, "mask bits");
@@ -183,6 +183,31 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
   const int r0 = G::SHIFT ? RT * vrow : RT * vrow + delta;   // this thread's rows r0 (qy 0) .. r0 + RT - 1
   // no ghost rows (and no decay of the need region) on the side shared with the cluster peer
   const bool sh_lo = G::CL && crank == 1, sh_hi = G::CL && crank == 0;
+  // CL: the warp that owns the row facing the peer — the only one that reads the
+  // peer's row and stores into the peer's slots.  It synchronises with the peer's
+  // boundary warp only: after a group in which it stores, every lane arrives
+  // (release, cluster scope) on the peer's handshake barrier of that group; before
+  // a group in which it reads the peer's row it waits for the peer's previous group.
+  // rank 0 stores after G1/G3 and reads in G1/G3, rank 1 stores after G0/G2 and reads
+  // in G0/G2, so each side's wait also keeps its next store behind the peer's reads
+  // of the old value, and neither side can lead by two groups (no phase aliasing).
+  const bool bwarp = G::CL && (crank == 0 ? vrow == G::PY / RT - 1 : vrow == 0);
+  const uint32_t hb_s = mb_s + 8u * G::S;
+  auto pair_arrive = [&](int g) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(hb_s + 8u * g), "r"((unsigned)(crank ^ 1)));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+  };
+  auto pair_wait = [&](int g, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nHW_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra HW_%=;\n}\n" ::"r"(hb_s + 8u * g),
+        "r"(parity)
+        : "memory");
+    sl_fuzz(320000u);
+  };
+  uint32_t step = 0;   // pair steps completed (CL handshake phase)
   const int64_t sz = p.sz;
 
   // pair steps at planes pp = p_begin, p_begin + 2, ... of parity qz = 0;
@@ -247,6 +272,9 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
 
   if (threadIdx.x == 0) {
     for (int k = 0; k < G::S; ++k) mbar_init3(mb_s + 8u * k);
+    if constexpr (G::CL)   // handshake barriers of the cluster pair: one per group, 32 arrivals (a warp)
+      for (int k = 0; k < 4; ++k)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 32;" ::"r"(mb_s + 8u * (G::S + k)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int k = 0; k < G::S - 2; ++k) issue(base + k);  // planes p_begin-2 .. p_begin+S-5
   }
@@ -357,6 +385,13 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
   auto group = [&]<int GI, int RP>(int pp) {
     constexpr int A = GI & 1;                      // rows A, A + 2
     constexpr int LAGG = GI >> 1;
+    if constexpr (G::CL) {
+      if (bwarp) {   // the peer's previous group (its stores into this CTA's slots) is complete
+        if (crank == 0 && A == 1) pair_wait(GI - 1, step & 1u);
+        if (crank == 1 && GI == 2) pair_wait(1, step & 1u);
+        if (crank == 1 && GI == 0 && step > 0) pair_wait(3, (step - 1u) & 1u);
+      }
+    }
     if (FORM == 1) {                               // next group's right-hand side in flight
       constexpr int NGI = (GI + 1) & 3;
       issue_f(NGI, GI == 0 ? pp : GI == 3 ? pp + 2 : pp - 1, NGI & 1);
@@ -498,6 +533,10 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
 #pragma unroll
       for (int h = 0; h < H; ++h) ld_row(pcs + (A + 2 * h) * G::PX, U[A + 2 * h][RC]);
     }
+    if constexpr (G::CL) {
+      // this group's stores into the peer's slots and reads of the peer's row are done
+      if (bwarp && (A == 1) == (crank == 0)) pair_arrive(GI);
+    }
   };
 
   // owned rows of a final plane (ring entry RE) -> dst; the non-finite check
@@ -530,13 +569,7 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
   // between colour groups: the block's warps — and with CL the cluster peer, whose
   // boundary row each group may read — must have published the previous group
   auto group_sync = [&] {
-    if constexpr (G::CL) {
-      sl_fuzz(300000u);
-      q1_cluster_sync();
-      sl_fuzz(310000u);
-    } else {
-      __syncthreads();
-    }
+    __syncthreads();   // CL: the cluster peer is ordered by the boundary warps' handshake
   };
   // one pair step per iteration (not unrolled: with four columns per lane a
   // second unrolled step made the loop outgrow the instruction cache —
@@ -571,13 +604,11 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
       issue(pp + G::S - 3);
     }
     group.template operator()<1, RP0>(pp);
-    // plane pp is final after G1.  With CL its global stores are issued after the barrier: a
-    // cluster arrive.release right behind them would wait for their acknowledgement
-    if constexpr (!G::CL) store_plane(pp, std::integral_constant<int, RP0>{});
+    // plane pp is final after G1
+    store_plane(pp, std::integral_constant<int, RP0>{});
 #if SL_FUZZ_BREAK != 1
     group_sync();
 #endif
-    if constexpr (G::CL) store_plane(pp, std::integral_constant<int, RP0>{});
     group.template operator()<2, RP0>(pp);
     // CL: the peer stores its boundary row of plane pp+2 into this CTA's slot
     // when its next G0 ends; this CTA's own TMA copy of that plane (which
@@ -595,6 +626,7 @@ __device__ __forceinline__ void q1col_body(const Params &p, const CUtensorMap &t
     for (int a = 0; a < RT; ++a)
 #pragma unroll
       for (int c = 0; c < C; ++c) U[a][0][c] = U[a][RP0][c];
+    ++step;
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // drain the copies issued but never waited for
