@@ -17,6 +17,11 @@
  *    :247-249) are reported by OR-ing SL_E_NONFINITE into *d_status
  *    (device int32, caller zeroes it); the caller reads it back after the
  *    stream has drained.  Grid contents after such an error are unspecified.
+ *    Bit 1 (value 2) of *d_status is set when the on-chip 2D sweep (one
+ *    cooperative launch for all sweeps, red-black grids that fit the chip)
+ *    gave up waiting for a neighbouring tile's exchange flag (a bounded
+ *    spin, so a broken co-residency assumption cannot hang the device); the
+ *    grid contents are then invalid too.
  *  - Return value: SL_OK, SL_E_INVAL (bad argument; reference ValueError),
  *    SL_E_UNSUPPORTED (stencil shape/weight pattern without a kernel) or
  *    SL_E_CUDA (launch error; see sl_last_cuda_error()).
